@@ -1,0 +1,378 @@
+"""Benchmark: compression-stage 1-bit LAMB step on a BERT-Large-shaped buffer.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N=1 runs one rank in-process; N>1 is launched by torchrun, one process per
+GPU, ranks exchanging packets over NCCL (weak scaling: every rank holds the
+full 336M-parameter replica and its own gradient, as in data parallelism).
+
+One "step" = Optimizer::step in the compression stage (optimizers.cpp:231-332):
+K1 worker compress -> alltoall -> K3 server reduce -> allgather -> K5/K6
+update.  `value` times K steps on device-resident gradients with CUDA events
+on the library's stream (max over ranks); `e2e` times the same step through
+the C-ABI with the gradient in pinned HOST memory (H2D copy + trace D2H inside
+the timed region).  The reference arm runs the reference library
+(oracle/_ref, fp64, OpenMP) on the host cores on a bounded sample of the same
+layout and extrapolates per parameter.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2104_06069_b200 import layouts  # noqa: E402
+
+METRIC = "1-bit LAMB compression-stage step time, BERT-Large params (336,226,108)"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def hbm_peak() -> tuple[float, str]:
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def grad_sigma(sizes, seed=1):
+    """Per-tensor gradient scale 10^(-4+2u) (SURVEY §8(d) synthetic inputs)."""
+    u = np.random.default_rng(seed).random(len(sizes))
+    return 10.0 ** (-4 + 2 * u)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in getattr(self, "lines", []):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes per launch
+# ---------------------------------------------------------------------------
+def algorithmic_bytes(d: int, n: int, nw: int) -> dict:
+    P = -(-d // n) * n
+    c = P // n
+    ns = nw
+    return {
+        # g (4d) + werr r/w (8P) + prev worker packet, prev result packet, new packet (3P/8)
+        "k1_worker_compress": nw * (4 * d + 8 * P + 3 * P / 8),
+        # serr r/w (8c) + n worker packets + prev server packet + new packet
+        "k3_server_reduce": ns * (8 * c + (n + 2) * c / 8),
+        # v r/w, vf (12d) + current and previous result bits (d/4)
+        "k5_update_a": 12 * d + d / 4,
+        # x r/w, vf (12d) + current result bits (d/8)
+        "k6_update_b": 12 * d + d / 8,
+    }
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the reference library on the host cores
+# ---------------------------------------------------------------------------
+def reference_sample(layout, n: int, target_params: int = 12_000_000, steps: int = 3):
+    """Time the reference's compression-stage Optimizer::step (oracle/_ref,
+    fp64, OpenMP over all host cores) on the leading tensors of `layout`
+    holding ~target_params parameters; returns seconds per step and the sample."""
+    from oracle import oracle as O
+
+    sizes, tot = [], 0
+    for _, s in layout:
+        if tot + s > target_params and sizes:
+            # take a slice of the next tensor so the sample hits the target
+            rest = target_params - tot
+            if rest > 1024:
+                sizes.append(rest)
+                tot += rest
+            break
+        sizes.append(s)
+        tot += s
+    d = tot
+    hp = O.HyperParams(total_steps=steps + 2, warmup_steps=1)
+    cl = O.Cluster("ref", n, d)
+    opt = O.Optimizer("ref", "onebit_lamb", sizes, hp)
+    rng = np.random.default_rng(1)
+    opt.set("x", rng.standard_normal(d) * 0.02)
+    sig = np.repeat(grad_sigma(sizes), sizes)
+    g = rng.standard_normal((n, d)) * sig
+    opt.step(g, 0, 1e-3, cl)  # warmup LAMB + freeze
+    opt.step(g, 1, 1e-3, cl)  # first compression step (untimed)
+    times = []
+    for t in range(steps):
+        t0 = time.perf_counter()
+        opt.step(g, 2 + t, 1e-3, cl)
+        times.append(time.perf_counter() - t0)
+    return float(np.median(times)), d, len(sizes)
+
+
+def cpu_cores() -> int:
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args, layout, d_full: int, n: int) -> dict:
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    s, d_s, L_s = reference_sample(layout, n, steps=max(1, min(args.steps, 3)))
+    ms = s * 1e3 * d_full / d_s
+    sample = (f"reference Optimizer::step (compression stage, n={n} simulated workers) on the "
+              f"first {L_s} BERT-Large tensors ({d_s:,} params), median of "
+              f"{max(1, min(args.steps, 3))} steps, extrapolated x{d_full / d_s:.2f} by parameter count")
+    return {"value": ms, "unit": "ms", "cores": cpu_cores(), "kind": "reference", "sample": sample}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="bert-large", choices=["bert-large", "bert-base", "config1"])
+    ap.add_argument("--sim-workers", type=int, default=0,
+                    help="simulate this many ranks on one GPU instead of one rank per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    layout = {"bert-large": layouts.bert_large, "bert-base": layouts.bert_base,
+              "config1": lambda: [(f"l{i}", s) for i, s in enumerate(layouts.CONFIG1)]}[args.workload]()
+    sizes = layouts.sizes(layout)
+    d = sum(sizes)
+    n = args.sim_workers if args.sim_workers else max(world, args.gpus if world == 1 else world)
+    if world == 1 and not args.sim_workers:
+        n = 1
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = run_reference(args, layout, d, n)
+        line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": "ms",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ref["value"], "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{args.workload} compression-stage step, n={n} workers",
+                           "params": d, "layers": len(sizes)},
+                "cpu_baseline": ref,
+                "e2e": {"value": ref["value"], "unit": "ms", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2104_06069_b200 import bitlamb as bl
+
+    stream = torch.cuda.Stream(device=local)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(bl.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local,
+                           nccl_unique_id=bytes(uid.cpu().numpy().tobytes()),
+                           stream=stream.cuda_stream)
+    else:
+        cl = bl.SimCluster(n, d, device=local, stream=stream.cuda_stream)
+    nw = cl.local_workers()
+    total_steps = 2 + args.warmup + 2 * args.steps + 8
+    hp = bl.HyperParams(total_steps=total_steps, warmup_steps=2)
+    opt = bl.Optimizer("onebit_lamb", layout, hp, cl)
+
+    # synthetic state and gradients (x0 ~ N(0, 0.02^2); g ~ N(0, sigma_l^2))
+    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    x0 = (torch.randn(d, generator=gen, device="cuda") * 0.02).cpu().numpy()
+    opt.set("x", x0)
+    sig = torch.from_numpy(np.repeat(grad_sigma(sizes), sizes).astype(np.float32)).cuda()
+    grads = torch.randn((nw, d), generator=gen, device="cuda") * sig
+    del sig
+    torch.cuda.synchronize()
+
+    # warm start: 2 warmup LAMB steps (freeze at the end), then compression steps
+    t = 0
+    for _ in range(2):
+        opt.step(grads, t, 1e-3)
+        t += 1
+    for _ in range(args.warmup):
+        opt.step(grads, t, 1e-3, trace=False)  # copies grads into the resident buffer
+        t += 1
+    cl.synchronize()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if not dist:
+            return v
+        tt = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    # ---- timed region: device-resident gradients ----
+    l0 = cl.kernel_launches()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            opt.step_resident(t, 1e-3)
+            t += 1
+        stop.record(stream)
+        stop.synchronize()
+    cl.synchronize()
+    barrier()
+    launches = (cl.kernel_launches() - l0) // args.steps
+    ms = max_over_ranks(start.elapsed_time(stop) / args.steps)
+
+    # ---- per-kernel breakdown (separate profiled pass, same steps) ----
+    cl.set_profiling(True)
+    for _ in range(args.steps):
+        opt.step_resident(t, 1e-3)
+        t += 1
+    prof = cl.profile()
+    cl.set_profiling(False)
+    kern = {k: {"ms_per_launch": v[0] / max(v[1], 1), "launches": v[1]} for k, v in prof.items()}
+    ab = algorithmic_bytes(d, cl.n_workers(), nw)
+    peak, peak_kind = hbm_peak()
+    dom = max((k for k in kern if k in ab), key=lambda k: kern[k]["ms_per_launch"] * kern[k]["launches"])
+    achieved = ab[dom] / (kern[dom]["ms_per_launch"] * 1e-3) / 1e9
+    for k in kern:
+        if k in ab:
+            kern[k]["gbs"] = ab[k] / (kern[k]["ms_per_launch"] * 1e-3) / 1e9
+    comm_ms = sum(kern.get(k, {}).get("ms_per_launch", 0) * kern.get(k, {}).get("launches", 0)
+                  for k in ("k1_worker_compress", "finalize_scales", "nccl_alltoall", "k3_server_reduce",
+                            "nccl_allgather")) / args.steps
+
+    # ---- e2e: reference-facing C-ABI call with pinned host gradients ----
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((nw, d), dtype=torch.float32, pin_memory=True)
+        host.copy_(grads)
+        ptrs = [host[i].data_ptr() for i in range(nw)]
+        opt.step_host_pointers(ptrs, t, 1e-3)  # warm
+        t += 1
+        barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            opt.step_host_pointers(ptrs, t, 1e-3)  # H2D + step + trace D2H (synchronous)
+            t += 1
+        e1.record(stream)
+        e1.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3 / args.steps
+        e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / args.steps, wall))
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 4 * d * nw,
+               "d2h_bytes_per_step": 4 * len(sizes) * 8 + 32}
+
+    del grads
+    torch.cuda.empty_cache()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = run_reference(args, layout, d, cl.n_workers())
+        except Exception as exc:  # reported, never silently replaced
+            cpu = {"error": f"{type(exc).__name__}: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC if args.workload == "bert-large" else f"1-bit LAMB step time, {args.workload}",
+            "value": ms, "unit": "ms", "n_gpus": args.gpus if world == 1 else world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.workload} 1-bit LAMB compression-stage step",
+                       "params": d, "layers": len(sizes), "world": cl.n_workers(),
+                       "mode": "nccl" if world > 1 else ("sim" if n > 1 else "single"),
+                       "parallelism": f"dp{cl.n_workers()}",
+                       "l2": "inputs larger than L2 (1.34 GB per state buffer vs 126 MB L2)"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "algorithmic_bytes": ab[dom]},
+            "kernels": kern,
+            "compressed_allreduce_ms": comm_ms,
+            "compressed_allreduce_algbw_gbs": 4 * d / (comm_ms * 1e-3) / 1e9 if comm_ms else None,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

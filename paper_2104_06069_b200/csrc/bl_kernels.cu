@@ -1,0 +1,1009 @@
+// bl_kernels.cu — hand-written sm_100a kernels of the 1-bit LAMB compression
+// stage (K1 worker compress, K3 server reduce, K5/K6 update, W1/W2 warmup) and
+// their small helpers.  Compiled with -fmad=false: the reference (x86-64, no
+// FMA) rounds every product and sum separately, and so must we.
+//
+// All sums accumulate in fp64 in the canonical tile-tree order (see
+// bl_kernels.cuh and oracle/bitlamb_oracle.c:tile_partial/combine_partials).
+// Per-element arithmetic follows the reference's evaluation order, cited at
+// each site (file:line relative to /root/reference/proj).
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "bl_kernels.cuh"
+
+namespace bl {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ float4 ld4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ float4 ld4_cs(const float* p) {
+  return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void st4_cs(float* p, float4 v) {
+  __stcs(reinterpret_cast<float4*>(p), v);
+}
+
+__device__ __forceinline__ float comp(const float4& v, int q) {
+  return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ void set_comp(float4& v, int q, float x) {
+  if (q == 0) v.x = x;
+  else if (q == 1) v.y = x;
+  else if (q == 2) v.z = x;
+  else v.w = x;
+}
+
+// row[4*lane .. 4*lane+3] where `row` may sit s = (row/4) % 4 floats past a
+// 16-byte boundary: aligned 128-bit loads plus a lane rotation.  All 32 lanes
+// must call it.  Reads up to 128+3 floats past `row - s` (buffers carry slack).
+template <bool STREAM>
+__device__ __forceinline__ float4 ld_row4(const float* row, int lane, int s) {
+  const float* a = row - s;
+  const float4 lo = STREAM ? ld4_cs(a + 4 * lane) : ld4(a + 4 * lane);
+  if (s == 0) return lo;
+  float hx = __shfl_down_sync(FULL, lo.x, 1);
+  float hy = __shfl_down_sync(FULL, lo.y, 1);
+  float hz = __shfl_down_sync(FULL, lo.z, 1);
+  if (lane == 31) {
+    const float4 h = ld4(a + 128);
+    hx = h.x;
+    hy = h.y;
+    hz = h.z;
+  }
+  if (s == 1) return make_float4(lo.y, lo.z, lo.w, hx);
+  if (s == 2) return make_float4(lo.z, lo.w, hx, hy);
+  return make_float4(lo.w, hx, hy, hz);
+}
+
+// Store the lane's nvalid (0..4) leading elements at row + 4*lane.
+__device__ __forceinline__ void st_row4(float* row, int lane, int s, const float4& v, int nvalid) {
+  float* p = row + 4 * lane;
+  if (s == 0 && nvalid >= 4) {
+    st4(p, v);
+    return;
+  }
+  if (nvalid > 0) p[0] = v.x;
+  if (nvalid > 1) p[1] = v.y;
+  if (nvalid > 2) p[2] = v.z;
+  if (nvalid > 3) p[3] = v.w;
+}
+
+__device__ __forceinline__ double warp_bfly_sum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const float w = __shfl_xor_sync(FULL, v, o);
+    v = v < w ? w : v;
+  }
+  return v;
+}
+
+// Canonical combine of per-thread stripe sums in a 1024-thread block
+// (oracle combine_partials).  Result valid in warp 0.
+__device__ __forceinline__ double block1024_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_bfly_sum(v);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (warp == 0) v = warp_bfly_sum(sh[lane]);
+  __syncthreads();
+  return v;
+}
+
+__device__ __forceinline__ float block1024_max(float v, float* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_max(v);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (warp == 0) v = warp_max(sh[lane]);
+  __syncthreads();
+  return v;
+}
+
+// Bits 4l..4l+3 of a chunk-aligned row: word 4r + l/8, nibble l%8.
+__device__ __forceinline__ uint32_t row_nibble(const uint32_t* words, int r, int lane) {
+  return (__ldg(words + 4 * r + (lane >> 3)) >> (4 * (lane & 7))) & 0xFu;
+}
+
+// Pack the lane nibbles of one row into 4 packet words (LSB-first).
+__device__ __forceinline__ void store_row_bits(uint32_t* words, int r, int lane, uint32_t nib) {
+  uint32_t v = nib << (4 * (lane & 7));
+  v |= __shfl_xor_sync(FULL, v, 1);
+  v |= __shfl_xor_sync(FULL, v, 2);
+  v |= __shfl_xor_sync(FULL, v, 4);
+  if ((lane & 7) == 0) words[4 * r + (lane >> 3)] = v;
+}
+
+__device__ __forceinline__ float slot_scale(const uint32_t* slot, uint64_t W) {
+  return __uint_as_float(__ldg(slot + W));
+}
+
+// Decompressed result value of a packet bit (compression.cpp:68-81):
+// scale == 0 -> +0, else bit ? +S : -S.
+__device__ __forceinline__ float dec_value(uint32_t bit, float S) {
+  return S == 0.0f ? 0.0f : (bit ? S : -S);
+}
+
+// Layer containing global element k (off[l] <= k < off[l+1]); L if k >= d.
+__device__ __forceinline__ int find_layer(const uint64_t* off, int L, uint64_t k) {
+  int lo = 0, hi = L;  // invariant: off[lo] <= k, answer in [lo, hi)
+  if (k >= __ldg(off + L)) return L;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(off + mid) <= k) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void flag(unsigned long long* err, int slot, unsigned long long key) {
+  if (err) atomicMin(err + slot, key);
+}
+
+// ---------------------------------------------------------------------------
+// K1 — worker compress (comm_sim.cpp:133-149 + compression.cpp:166-198 and,
+// in modes 1/2, the stream build of optimizers.cpp:248-255).
+//
+// MODE 0: stream = in[w] (SimCluster::compressed_allreduce API)
+// MODE 1: stream = A_l*m + B_l*g_w with m from the momentum buffer
+// MODE 2: stream = A_l*m + B_l*g_w with m = decompressed previous result *
+//         invc_l (m is never stored during the compression stage: after every
+//         step m == m_g, optimizers.cpp:315-319, which the packets encode).
+//
+// Deferred residual: werr holds raw = v + delta (compression.cpp:194-195
+// before the reconstruction is subtracted); delta = raw - (bit ? S : -S) is
+// materialised from the previous packet when read.  Identical arithmetic,
+// one pass: 12 B/elem read + 4 B/elem written + 1 bit.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k1_worker_compress(const K1Params p) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const long long per_w = static_cast<long long>(p.n) * p.tpc;
+  const long long total = per_w * p.nw;
+  const float es = p.es_dev ? __ldg(p.es_dev) : p.es_host;
+
+  for (long long tile = gw; tile < total; tile += nwarps) {
+    const int w = static_cast<int>(tile / per_w);
+    const long long rem = tile - w * per_w;
+    const int j = static_cast<int>(rem / p.tpc);
+    const int t = static_cast<int>(rem - static_cast<long long>(j) * p.tpc);
+    const uint64_t i0 = static_cast<uint64_t>(t) * kTile;  // chunk-relative
+    const uint64_t kc = static_cast<uint64_t>(j) * p.c;    // global chunk start
+    const int s = static_cast<int>(kc & 3u);
+    const size_t ep = static_cast<size_t>(w) * p.n + j;    // endpoint (worker, chunk)
+    const float* gin = p.in + static_cast<size_t>(w) * p.in_stride + kc + i0;
+    float* we = p.werr + ep * p.c_pad + i0;
+    const uint32_t* pkp = p.pk_prev + ep * p.slot;
+    uint32_t* pkc = p.pk_cur + ep * p.slot + (i0 >> 5);
+    const float Sp = slot_scale(pkp, p.W);
+    pkp += i0 >> 5;
+
+    float pos_m = 0.f, neg_m = 0.f;
+    const uint32_t* rp = nullptr;
+    if (MODE == 2) {
+      const uint32_t* rs = p.res_prev + static_cast<size_t>(j) * p.slot;
+      const float S2 = slot_scale(rs, p.W);
+      pos_m = S2;
+      neg_m = S2 == 0.0f ? 0.0f : -S2;
+      rp = rs + (i0 >> 5);
+    }
+    int l = 0;
+    float A = 0.f, B = 0.f, IC = 0.f;
+    int lcache = -1;
+    if (MODE != 0) l = find_layer(p.off, p.L, kc + i0);
+
+    double acc = 0.0;
+    float cm = 0.0f;
+    for (int r = 0; r < kRowsPerTile; ++r) {
+      const uint64_t ir = i0 + static_cast<uint64_t>(r) * kRowElems;
+      if (ir >= p.c) break;
+      const uint64_t kr = kc + ir;
+      const float4 g = ld_row4<true>(gin + r * kRowElems, lane, s);
+      float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (MODE == 1) mv = ld_row4<false>(p.m + kr, lane, s);
+      const float4 raw = ld4(we + r * kRowElems + 4 * lane);
+      const uint32_t wnib = row_nibble(pkp, r, lane);
+      uint32_t rnib = 0;
+      if (MODE == 2) rnib = row_nibble(rp, r, lane);
+
+      // Stream value for each of the lane's 4 elements.
+      float4 sv;
+      if (MODE == 0) {
+        sv = g;
+      } else {
+        while (l < p.L && kr >= __ldg(p.off + l + 1)) ++l;
+        const bool uniform = l < p.L && kr + (kRowElems - 1) < __ldg(p.off + l + 1);
+        if (uniform && l != lcache) {
+          A = __ldg(p.A + l);
+          B = __ldg(p.B + l);
+          IC = __ldg(p.invc + l);
+          lcache = l;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float a = A, b = B, ic = IC;
+          bool pad = false;
+          if (!uniform) {
+            const uint64_t k = kr + 4 * lane + q;
+            int le = l;
+            while (le < p.L && k >= __ldg(p.off + le + 1)) ++le;
+            pad = le >= p.L;
+            if (!pad) {
+              a = __ldg(p.A + le);
+              b = __ldg(p.B + le);
+              ic = __ldg(p.invc + le);
+            }
+          }
+          float mq;
+          if (MODE == 1) mq = comp(mv, q);
+          else mq = __fmul_rn((rnib >> q) & 1u ? pos_m : neg_m, ic);  // fusion.cpp:143
+          // kernels.cpp:253  dst = a*x + b*y
+          const float v = pad ? 0.0f : __fadd_rn(__fmul_rn(a, mq), __fmul_rn(b, comp(g, q)));
+          set_comp(sv, q, v);
+        }
+      }
+      if (MODE != 0) {
+        // check_gradients (optimizers.cpp:99-117): flag, reported by the host.
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint64_t k = kr + 4 * lane + q;
+          if (ir + 4 * lane + q < p.c && k < p.d && !isfinite(comp(g, q))) {
+            flag(p.err, kErrGrad,
+                 (static_cast<unsigned long long>(p.worker_base + w) << 40) | k);
+          }
+        }
+      }
+
+      uint32_t nib = 0;
+      float4 rawn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t i = ir + 4 * lane + q;
+        const uint64_t k = kc + i;
+        const float v = k < p.d ? comp(sv, q) : 0.0f;  // comm_sim.cpp:136-137 zero pad
+        const float rec = (wnib >> q) & 1u ? Sp : -Sp;
+        const float delta = __fsub_rn(comp(raw, q), rec);          // compression.cpp:194-195
+        const float corr = __fadd_rn(v, __fmul_rn(es, delta));     // :181 (1*v + es*delta)
+        const float rn = __fadd_rn(v, delta);                      // v + delta
+        const bool live = i < p.c;
+        set_comp(rawn, q, live ? rn : 0.0f);
+        if (live) {
+          nib |= static_cast<uint32_t>(corr >= 0.0f) << q;         // compression.cpp:50
+          acc += fabs(static_cast<double>(corr));                   // :54 sum_abs
+          const float ac = fabsf(corr);
+          cm = cm < ac ? ac : cm;
+        }
+      }
+      st4(we + r * kRowElems + 4 * lane, rawn);
+      store_row_bits(pkc, r, lane, nib);
+    }
+    acc = warp_bfly_sum(acc);
+    if (lane == 0) p.partials[ep * p.tpc + t] = acc;
+    if (p.cmax) {
+      cm = warp_max(cm);
+      if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
+    }
+  }
+}
+
+// Scale of each endpoint: S = (float)(sum|corrected| / c) (compression.cpp:54-55),
+// non-finite -> flag (compression.cpp:56-58).  One 1024-thread block per endpoint.
+__global__ void __launch_bounds__(1024) k_finalize_scales(const FinalizeParams p) {
+  __shared__ double sh[32];
+  const int e = blockIdx.x;
+  const double* part = p.partials + static_cast<size_t>(e) * p.tpc;
+  double s = 0.0;
+  for (int t = threadIdx.x; t < p.tpc; t += 1024) s += part[t];
+  s = block1024_sum(s, sh);
+  if (threadIdx.x == 0) {
+    const float S = static_cast<float>(s / static_cast<double>(p.c));
+    p.slots[static_cast<size_t>(e) * p.slot_stride + p.W] = __float_as_uint(S);
+    if (!isfinite(S)) flag(p.err, kErrScale, static_cast<unsigned long long>(p.err_base + e));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 — server reduce (comm_sim.cpp:158-181): ascending-worker average of the
+// n one-bit messages (compression.cpp:83-89, skipped when S == 0; scale 1/n in
+// fp64, :164), error-compensated recompression with the server residual.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
+  __shared__ float s_scale[kWarpsPerBlock][64];
+  const int n = NT > 0 ? NT : p.n;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const long long total = static_cast<long long>(p.ns) * p.tpc;
+  const float es = p.es_dev ? __ldg(p.es_dev) : p.es_host;
+  const double inv_n = 1.0 / static_cast<double>(n);
+
+  for (long long tile = gw; tile < total; tile += nwarps) {
+    const int sv = static_cast<int>(tile / p.tpc);
+    const int t = static_cast<int>(tile - static_cast<long long>(sv) * p.tpc);
+    const int j = p.server_base + sv;
+    const uint64_t i0 = static_cast<uint64_t>(t) * kTile;
+    const uint32_t* in = p.in + sv * p.in_s;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) s_scale[wib][i] = slot_scale(in + i * p.in_i, p.W);
+    __syncwarp();
+    float* se = p.serr + static_cast<size_t>(sv) * p.c_pad + i0;
+    const uint32_t* rs = p.res_prev + static_cast<size_t>(j) * p.slot;
+    const float S2p = slot_scale(rs, p.W);
+    rs += i0 >> 5;
+    uint32_t* rc = p.res_cur + static_cast<size_t>(j) * p.slot + (i0 >> 5);
+    const uint32_t* inw = in + (i0 >> 5);
+
+    double acc = 0.0;
+    float cm = 0.0f;
+    for (int r = 0; r < kRowsPerTile; ++r) {
+      const uint64_t ir = i0 + static_cast<uint64_t>(r) * kRowElems;
+      if (ir >= p.c) break;
+      const float4 raw = ld4(se + r * kRowElems + 4 * lane);
+      const uint32_t snib = row_nibble(rs, r, lane);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll(NT > 0 ? NT : 1)
+      for (int i = 0; i < n; ++i) {
+        const float S = s_scale[wib][i];
+        const uint32_t nb = row_nibble(inw + i * p.in_i, r, lane);
+        if (S != 0.0f) {
+          const double Sd = S;
+          a0 += (nb & 1u) ? Sd : -Sd;
+          a1 += (nb & 2u) ? Sd : -Sd;
+          a2 += (nb & 4u) ? Sd : -Sd;
+          a3 += (nb & 8u) ? Sd : -Sd;
+        }
+      }
+      const float4 avg = make_float4(static_cast<float>(a0 * inv_n), static_cast<float>(a1 * inv_n),
+                                     static_cast<float>(a2 * inv_n), static_cast<float>(a3 * inv_n));
+      uint32_t nib = 0;
+      float4 rawn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t i = ir + 4 * lane + q;
+        const float v = comp(avg, q);
+        const float rec = (snib >> q) & 1u ? S2p : -S2p;
+        const float delta = __fsub_rn(comp(raw, q), rec);
+        const float corr = __fadd_rn(v, __fmul_rn(es, delta));
+        const float rn = __fadd_rn(v, delta);
+        const bool live = i < p.c;
+        set_comp(rawn, q, live ? rn : 0.0f);
+        if (live) {
+          nib |= static_cast<uint32_t>(corr >= 0.0f) << q;
+          acc += fabs(static_cast<double>(corr));
+          const float ac = fabsf(corr);
+          cm = cm < ac ? ac : cm;
+        }
+      }
+      st4(se + r * kRowElems + 4 * lane, rawn);
+      store_row_bits(rc, r, lane, nib);
+    }
+    acc = warp_bfly_sum(acc);
+    if (lane == 0) p.partials[static_cast<size_t>(sv) * p.tpc + t] = acc;
+    if (p.cmax) {
+      cm = warp_max(cm);
+      if (lane == 0) p.cmax[static_cast<size_t>(sv) * p.tpc + t] = cm;
+    }
+  }
+}
+
+// Result bits of 4 consecutive global elements k0..k0+3 from chunk-relative
+// packets; (j, chunk_end) track the chunk of the row start.
+struct BitCursor {
+  const uint32_t* res;
+  uint64_t c, slot, W;
+  int n;
+};
+
+__device__ __forceinline__ uint32_t bit_at(const BitCursor& bc, uint64_t k, float* S) {
+  uint64_t j = k / bc.c;
+  if (j >= static_cast<uint64_t>(bc.n)) j = bc.n - 1;
+  const uint64_t i = k - j * bc.c;
+  const uint32_t* sl = bc.res + j * bc.slot;
+  *S = slot_scale(sl, bc.W);
+  return (__ldg(sl + (i >> 5)) >> (i & 31)) & 1u;
+}
+
+// Values m_g = dec * invc for the lane's 4 elements of a layer row starting at
+// global kr (fusion.cpp:139-145 applied to compression.cpp:68-81).
+__device__ __forceinline__ float4 row_mg(const BitCursor& bc, uint64_t kr, int lane, float ic,
+                                         uint64_t& j, uint64_t& chunk_end) {
+  while (kr >= chunk_end) {
+    ++j;
+    chunk_end += bc.c;
+  }
+  float4 out;
+  if (kr + (kRowElems - 1) < chunk_end || j + 1 >= static_cast<uint64_t>(bc.n)) {
+    const uint32_t* sl = bc.res + j * bc.slot;
+    const float S = slot_scale(sl, bc.W);
+    const float pos = S, neg = S == 0.0f ? 0.0f : -S;
+    const uint64_t i = kr - j * bc.c + 4 * lane;
+    const uint64_t wi = i >> 5;
+    const uint32_t w0 = __ldg(sl + wi), w1 = __ldg(sl + wi + 1);
+    const uint32_t nib = __funnelshift_r(w0, w1, static_cast<uint32_t>(i & 31)) & 0xFu;
+    out.x = __fmul_rn(nib & 1u ? pos : neg, ic);
+    out.y = __fmul_rn(nib & 2u ? pos : neg, ic);
+    out.z = __fmul_rn(nib & 4u ? pos : neg, ic);
+    out.w = __fmul_rn(nib & 8u ? pos : neg, ic);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float S;
+      const uint32_t b = bit_at(bc, kr + 4 * lane + q, &S);
+      set_comp(out, q, __fmul_rn(dec_value(b, S), ic));
+    }
+  }
+  return out;
+}
+
+__device__ __forceinline__ int lane_valid(uint64_t len, uint64_t ir, int lane) {
+  const uint64_t st = ir + 4 * lane;
+  if (st >= len) return 0;
+  const uint64_t rem = len - st;
+  return rem >= 4 ? 4 : static_cast<int>(rem);
+}
+
+// ---------------------------------------------------------------------------
+// K5 — update pass A (optimizers.cpp:271-300): reconstruct the averaged
+// gradient from the momentum recurrence, refresh the live variance, per-layer
+// ratio max (kernels.cpp:185-198) and ||v||^2 trace partials.
+// MPREV 0: m_prev from the momentum buffer (first step after the freeze);
+// MPREV 1: m_prev from the previous result packets.
+// ---------------------------------------------------------------------------
+template <int MPREV>
+__global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const BitCursor cur{p.res_cur, p.c, p.slot, p.W, p.n};
+  const BitCursor prv{p.res_prev, p.c, p.slot, p.W, p.n};
+
+  for (long long tile = gw; tile < p.lt.tiles; tile += nwarps) {
+    const int l = __ldg(p.lt.tile_layer + tile);
+    const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
+    const uint64_t lo = __ldg(p.lt.off + l);
+    const uint64_t len = __ldg(p.lt.off + l + 1) - lo;
+    const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
+    const int s = static_cast<int>(lo & 3u);
+    const float ic = __ldg(p.invc + l);
+    uint64_t j = base / p.c, ce = (j + 1) * p.c;
+    uint64_t jp = j, cep = ce;
+
+    double acc = 0.0;
+    float mx = 0.0f;
+    bool bad = false;
+    for (int r = 0; r < kRowsPerTile; ++r) {
+      const uint64_t ir = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r) * kRowElems;
+      if (ir >= len) break;
+      const uint64_t kr = base + static_cast<uint64_t>(r) * kRowElems;
+      const int nv = lane_valid(len, ir, lane);
+      const float4 v = ld_row4<false>(p.v + kr, lane, s);
+      const float4 vf = ld_row4<false>(p.vf + kr, lane, s);
+      const float4 mg = row_mg(cur, kr, lane, ic, j, ce);
+      float4 mp;
+      if (MPREV == 0) mp = ld_row4<false>(p.m + kr, lane, s);
+      else mp = row_mg(prv, kr, lane, ic, jp, cep);
+      float4 vn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        // :284-287 rec = inv*m_g + (-beta1*inv)*m_prev
+        const float rec = __fadd_rn(__fmul_rn(p.inv, comp(mg, q)), __fmul_rn(p.ninvb, comp(mp, q)));
+        // kernels.cpp:245 y = a*y + b*x*x
+        const float nvv = __fadd_rn(__fmul_rn(p.b2, comp(v, q)),
+                                    __fmul_rn(__fmul_rn(p.omb2, rec), rec));
+        set_comp(vn, q, nvv);
+        if (q < nv) {
+          bad |= !isfinite(rec);
+          const float den = nvv < p.floor_ ? p.floor_ : nvv;  // std::max(v, floor)
+          const float ratio = fabsf(comp(vf, q)) / den;
+          mx = mx < ratio ? ratio : mx;
+          acc += static_cast<double>(nvv) * static_cast<double>(nvv);
+        }
+      }
+      st_row4(p.v + kr, lane, s, vn, nv);
+    }
+    if (bad) flag(p.err, kErrRecon, static_cast<unsigned long long>(l));
+    acc = warp_bfly_sum(acc);
+    mx = warp_max(mx);
+    if (lane == 0) {
+      p.tile_v2[tile] = acc;
+      p.tile_max[tile] = mx;
+    }
+  }
+}
+
+// Per-layer epilogue between K5 and K6 (optimizers.cpp:296-300, 317, 321-330):
+// one 1024-thread block per layer; the last block also advances the
+// c_mean history (:328-330) and the experimental error scale (:226-229).
+__global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
+  __shared__ double shd[32];
+  __shared__ float shf[32];
+  __shared__ bool last;
+  const int l = blockIdx.x;
+  const int t0 = p.layer_tile_start[l], t1 = p.layer_tile_start[l + 1];
+  double s = 0.0;
+  float mx = 0.0f;
+  for (int t = t0 + threadIdx.x; t < t1; t += 1024) {
+    s += p.tile_v2[t];
+    const float m = p.tile_max[t];
+    mx = mx < m ? m : mx;
+  }
+  s = block1024_sum(s, shd);
+  mx = block1024_max(mx, shf);
+  if (threadIdx.x == 0) {
+    const int L = p.L;
+    const double pre = static_cast<double>(mx);
+    const double rp = p.r_prev[l];
+    // vector_ops.cpp:25-28 clip = min(max(x, a), b)
+    const double lo1 = (1.0 - p.r_thr) * rp, hi1 = (1.0 + p.r_thr) * rp;
+    double r = pre < lo1 ? lo1 : pre;
+    r = hi1 < r ? hi1 : r;
+    r = r < p.r_min ? p.r_min : r;
+    r = p.r_max < r ? p.r_max : r;
+    const double c = r * p.c_avg[l];
+    p.r_prev[l] = r;
+    p.coef_x[l] = static_cast<float>(-p.lr * c);
+    p.trace[l] = c;
+    p.trace[L + l] = r;
+    p.trace[2 * L + l] = sqrt(s);
+    p.trace[3 * L + l] = pre;
+    __threadfence();
+    last = atomicAdd(p.counter, 1u) == static_cast<unsigned>(L - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* tr = p.trace;
+    double c_sum = 0.0;
+    for (int k = 0; k < p.L; ++k) c_sum += tr[k];
+    p.cmean[1] = p.cmean[0];
+    const double cm = c_sum / static_cast<double>(p.L);
+    p.cmean[0] = cm < p.floor_ ? p.floor_ : cm;
+    *p.es_next = p.scaled_ef ? static_cast<float>(p.cmean[1] / p.cmean[0]) : 1.0f;
+    *p.counter = 0u;
+  }
+}
+
+// K6 — update pass B (optimizers.cpp:308-313): u = m_g/(sqrt(vf)+eta) [+wd x],
+// x += (-lr*c)*u, with m_g recomputed from the result packets.
+__global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const BitCursor cur{p.res_cur, p.c, p.slot, p.W, p.n};
+  for (long long tile = gw; tile < p.lt.tiles; tile += nwarps) {
+    const int l = __ldg(p.lt.tile_layer + tile);
+    const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
+    const uint64_t lo = __ldg(p.lt.off + l);
+    const uint64_t len = __ldg(p.lt.off + l + 1) - lo;
+    const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
+    const int s = static_cast<int>(lo & 3u);
+    const float ic = __ldg(p.invc + l);
+    const float a = __ldg(p.coef_x + l);
+    uint64_t j = base / p.c, ce = (j + 1) * p.c;
+    for (int r = 0; r < kRowsPerTile; ++r) {
+      const uint64_t ir = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r) * kRowElems;
+      if (ir >= len) break;
+      const uint64_t kr = base + static_cast<uint64_t>(r) * kRowElems;
+      const int nv = lane_valid(len, ir, lane);
+      const float4 x = ld_row4<false>(p.x + kr, lane, s);
+      const float4 vf = ld_row4<false>(p.vf + kr, lane, s);
+      const float4 mg = row_mg(cur, kr, lane, ic, j, ce);
+      float4 xn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        // kernels.cpp:229 precondition: m / (sqrt(v) + eta)
+        float u = __fdiv_rn(comp(mg, q), __fadd_rn(__fsqrt_rn(comp(vf, q)), p.eta));
+        if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x, q)));  // kernels.cpp:226 axpy
+        set_comp(xn, q, __fadd_rn(comp(x, q), __fmul_rn(a, u)));          // :313 axpy
+      }
+      st_row4(p.x + kr, lane, s, xn, nv);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warmup stage (optimizers.cpp:140-177 lamb_step / :179-200 adam_step).
+// W1: m, v update; tile partials of ||x||^2 (pre-update), ||u||^2, ||v||^2 and
+// sum|m| (compute_scales, fusion.cpp:107-125, used when the stage ends).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long tile = gw; tile < p.lt.tiles; tile += nwarps) {
+    const int l = __ldg(p.lt.tile_layer + tile);
+    const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
+    const uint64_t lo = __ldg(p.lt.off + l);
+    const uint64_t len = __ldg(p.lt.off + l + 1) - lo;
+    const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
+    const int s = static_cast<int>(lo & 3u);
+    double ax = 0.0, au = 0.0, av = 0.0, am = 0.0;
+    for (int r = 0; r < kRowsPerTile; ++r) {
+      const uint64_t ir = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r) * kRowElems;
+      if (ir >= len) break;
+      const uint64_t kr = base + static_cast<uint64_t>(r) * kRowElems;
+      const int nv = lane_valid(len, ir, lane);
+      const float4 g = ld_row4<false>(p.gbar + kr, lane, s);
+      const float4 m = ld_row4<false>(p.m + kr, lane, s);
+      const float4 v = ld_row4<false>(p.v + kr, lane, s);
+      const float4 x = ld_row4<false>(p.x + kr, lane, s);
+      float4 mn, vn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float gq = comp(g, q);
+        // kernels.cpp:238 axpby y = a*y + b*x ; :245 axpby_square
+        const float mq = __fadd_rn(__fmul_rn(p.b1, comp(m, q)), __fmul_rn(p.omb1, gq));
+        const float vq = __fadd_rn(__fmul_rn(p.b2, comp(v, q)), __fmul_rn(__fmul_rn(p.omb2, gq), gq));
+        set_comp(mn, q, mq);
+        set_comp(vn, q, vq);
+        if (q < nv) {
+          float u = __fdiv_rn(mq, __fadd_rn(__fsqrt_rn(vq), p.eta));
+          if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x, q)));
+          const double xd = comp(x, q), ud = u, vd = vq;
+          ax += xd * xd;
+          au += ud * ud;
+          av += vd * vd;
+          am += fabs(static_cast<double>(mq));
+        }
+      }
+      st_row4(p.m + kr, lane, s, mn, nv);
+      st_row4(p.v + kr, lane, s, vn, nv);
+    }
+    ax = warp_bfly_sum(ax);
+    au = warp_bfly_sum(au);
+    av = warp_bfly_sum(av);
+    am = warp_bfly_sum(am);
+    if (lane == 0) {
+      double* ts = p.tile_sums + 4 * tile;
+      ts[0] = ax;
+      ts[1] = au;
+      ts[2] = av;
+      ts[3] = am;
+    }
+  }
+}
+
+// Warmup epilogue: per-layer coefficient (optimizers.cpp:158-172) and, at
+// the end of the stage, finalize_warmup (:202-224) in the last block.
+__global__ void __launch_bounds__(1024) k_wepilogue(const WEpiParams p) {
+  __shared__ double shd[32];
+  __shared__ bool last;
+  const int l = blockIdx.x;
+  const int t0 = p.layer_tile_start[l], t1 = p.layer_tile_start[l + 1];
+  double sx = 0.0, su = 0.0, sv = 0.0, sm = 0.0;
+  for (int t = t0 + threadIdx.x; t < t1; t += 1024) {
+    sx += p.tile_sums[4 * t + 0];
+    su += p.tile_sums[4 * t + 1];
+    sv += p.tile_sums[4 * t + 2];
+    sm += p.tile_sums[4 * t + 3];
+  }
+  sx = block1024_sum(sx, shd);
+  su = block1024_sum(su, shd);
+  sv = block1024_sum(sv, shd);
+  sm = block1024_sum(sm, shd);
+  if (threadIdx.x == 0) {
+    const int L = p.L;
+    double c = 1.0;
+    if (!p.adam) {
+      const double xn = sqrt(sx), un = sqrt(su);
+      auto clip = [](double x, double a, double b) {
+        const double y = x < a ? a : x;
+        return b < y ? b : y;
+      };
+      if (un == 0.0) c = xn > 0.0 ? p.c_max : clip(1.0, p.c_min, p.c_max);
+      else c = clip(xn / un, p.c_min, p.c_max);
+      p.coef_x[l] = static_cast<float>(-p.lr * c);
+      if (p.track) p.c_avg[l] = p.b3 * p.c_avg[l] + (1.0 - p.b3) * c;
+    } else {
+      p.coef_x[l] = static_cast<float>(-p.lr);
+    }
+    p.trace[l] = c;
+    p.trace[L + l] = 1.0;
+    p.trace[2 * L + l] = sqrt(sv);
+    p.trace[3 * L + l] = 1.0;
+    if (p.finalize) {
+      const double len = static_cast<double>(p.off[l + 1] - p.off[l]);
+      const double mean = sm / len;                     // vector_ops.cpp:41-44 mean_abs
+      p.mag[l] = mean < p.floor_ ? p.floor_ : mean;     // fusion.cpp:116
+    }
+    __threadfence();
+    last = atomicAdd(p.counter, 1u) == static_cast<unsigned>(L - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    if (p.finalize) {
+      const volatile double* mag = p.mag;
+      const volatile double* cav = p.c_avg;
+      if (!p.onebit_adam) {
+        double ref = 0.0;
+        for (int k = 0; k < p.L; ++k) ref += mag[k];
+        ref /= static_cast<double>(p.L);
+        for (int k = 0; k < p.L; ++k) p.coeff[k] = ref / mag[k];
+      } else {
+        for (int k = 0; k < p.L; ++k) p.coeff[k] = 1.0;
+      }
+      double c_mean = 0.0;
+      for (int k = 0; k < p.L; ++k) c_mean += p.onebit_adam ? 1.0 : cav[k];
+      c_mean /= static_cast<double>(p.L);
+      const double cm = c_mean < p.floor_ ? p.floor_ : c_mean;
+      p.cmean[0] = cm;
+      p.cmean[1] = cm;
+      *p.es_next = 1.0f;
+      for (int k = 0; k < p.L; ++k) {
+        const double co = p.coeff[k];
+        p.A[k] = static_cast<float>(co * p.b1);          // optimizers.cpp:252
+        p.B[k] = static_cast<float>(co * (1.0 - p.b1));  // :253
+        p.invc[k] = static_cast<float>(1.0 / co);        // fusion.cpp:143
+      }
+    }
+    *p.counter = 0u;
+  }
+}
+
+// W2: u = m/(sqrt(v)+eta) [+wd x]; x += (-lr*c)*u; at the freeze vf = v.
+__global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long tile = gw; tile < p.lt.tiles; tile += nwarps) {
+    const int l = __ldg(p.lt.tile_layer + tile);
+    const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
+    const uint64_t lo = __ldg(p.lt.off + l);
+    const uint64_t len = __ldg(p.lt.off + l + 1) - lo;
+    const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
+    const int s = static_cast<int>(lo & 3u);
+    const float a = __ldg(p.coef_x + l);
+    for (int r = 0; r < kRowsPerTile; ++r) {
+      const uint64_t ir = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r) * kRowElems;
+      if (ir >= len) break;
+      const uint64_t kr = base + static_cast<uint64_t>(r) * kRowElems;
+      const int nv = lane_valid(len, ir, lane);
+      const float4 m = ld_row4<false>(p.m + kr, lane, s);
+      const float4 v = ld_row4<false>(p.v + kr, lane, s);
+      const float4 x = ld_row4<false>(p.x + kr, lane, s);
+      float4 xn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float u = __fdiv_rn(comp(m, q), __fadd_rn(__fsqrt_rn(comp(v, q)), p.eta));
+        if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x, q)));
+        set_comp(xn, q, __fadd_rn(comp(x, q), __fmul_rn(a, u)));
+      }
+      st_row4(p.x + kr, lane, s, xn, nv);
+      if (p.finalize) st_row4(p.vf + kr, lane, s, v, nv);  // optimizers.cpp:205
+    }
+  }
+}
+
+// Lossless average (comm_sim.cpp:214-222): ascending workers in fp64, * 1/n.
+__global__ void k_average(const float* in, uint64_t stride, int n, uint64_t len, float* out,
+                          unsigned long long* err, int check, int worker_base) {
+  const double inv_n = 1.0 / static_cast<double>(n);
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const float g = __ldcs(in + static_cast<size_t>(i) * stride + k);
+      if (check && !isfinite(g))
+        flag(err, kErrGrad, (static_cast<unsigned long long>(worker_base + i) << 40) | k);
+      acc += static_cast<double>(g);
+    }
+    if (out) out[k] = static_cast<float>(acc * inv_n);
+  }
+}
+
+__global__ void k_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
+                             uint64_t d, float* out) {
+  const BitCursor bc{res, c, slot, W, n};
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < d;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    float S;
+    const uint32_t b = bit_at(bc, k, &S);
+    out[k] = dec_value(b, S);
+  }
+}
+
+__global__ void k_materialize_error(const float* raw, uint64_t c_pad, const uint32_t* pk,
+                                    uint64_t slot, uint64_t W, uint64_t c, uint64_t len,
+                                    float* out) {
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t j = k / c, i = k - j * c;
+    const uint32_t* sl = pk + j * slot;
+    const float S = slot_scale(sl, W);
+    const uint32_t b = (__ldg(sl + (i >> 5)) >> (i & 31)) & 1u;
+    out[k] = __fsub_rn(raw[j * c_pad + i], b ? S : -S);
+  }
+}
+
+__global__ void k_materialize_m(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
+                                const uint64_t* off, int L, const float* invc, uint64_t d,
+                                float* out) {
+  const BitCursor bc{res, c, slot, W, n};
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < d;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    float S;
+    const uint32_t b = bit_at(bc, k, &S);
+    const int l = find_layer(off, L, k);
+    out[k] = __fmul_rn(dec_value(b, S), __ldg(invc + l));
+  }
+}
+
+// Flat-order statistics of a materialised residual: tile partials of
+// sum delta^2 and max|delta| (one warp per 4096 flat tile).
+__global__ void __launch_bounds__(kBlock) k_error_stats_tiles(
+    const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot, uint64_t W, uint64_t c,
+    uint64_t len, double* part, float* pmax, int tiles) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long tile = gw; tile < tiles; tile += nwarps) {
+    double acc = 0.0;
+    float mx = 0.0f;
+    for (int r = 0; r < kRowsPerTile; ++r) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t k = static_cast<uint64_t>(tile) * kTile + r * kRowElems + 4 * lane + q;
+        if (k < len) {
+          const uint64_t j = k / c, i = k - j * c;
+          const uint32_t* sl = pk + j * slot;
+          const float S = slot_scale(sl, W);
+          const uint32_t b = (__ldg(sl + (i >> 5)) >> (i & 31)) & 1u;
+          const float dlt = __fsub_rn(raw[j * c_pad + i], b ? S : -S);
+          acc += static_cast<double>(dlt) * static_cast<double>(dlt);
+          const float a = fabsf(dlt);
+          mx = mx < a ? a : mx;
+        }
+      }
+    }
+    acc = warp_bfly_sum(acc);
+    mx = warp_max(mx);
+    if (lane == 0) {
+      part[tile] = acc;
+      pmax[tile] = mx;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_error_stats_final(const double* part, const float* pmax,
+                                                            int tiles, double* out) {
+  __shared__ double shd[32];
+  __shared__ float shf[32];
+  double s = 0.0;
+  float mx = 0.0f;
+  for (int t = threadIdx.x; t < tiles; t += 1024) {
+    s += part[t];
+    mx = mx < pmax[t] ? pmax[t] : mx;
+  }
+  s = block1024_sum(s, shd);
+  mx = block1024_max(mx, shf);
+  if (threadIdx.x == 0) {
+    out[0] = s;
+    out[1] = mx;
+  }
+}
+
+__global__ void k_set_float(float* p, float v) { *p = v; }
+
+int grid_for_elems(uint64_t n) {
+  const uint64_t g = (n + 255) / 256;
+  return static_cast<int>(g < 148 * 16 ? (g == 0 ? 1 : g) : 148 * 16);
+}
+
+}  // namespace
+
+int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
+  switch (mode) {
+    case 0: k1_worker_compress<0><<<grid, kBlock, 0, s>>>(p); break;
+    case 1: k1_worker_compress<1><<<grid, kBlock, 0, s>>>(p); break;
+    default: k1_worker_compress<2><<<grid, kBlock, 0, s>>>(p); break;
+  }
+  return 1;
+}
+
+int launch_finalize(const FinalizeParams& p, int count, cudaStream_t s) {
+  k_finalize_scales<<<count, 1024, 0, s>>>(p);
+  return 1;
+}
+
+int launch_k3(const K3Params& p, int grid, cudaStream_t s) {
+  switch (p.n) {
+    case 1: k3_server_reduce<1><<<grid, kBlock, 0, s>>>(p); break;
+    case 2: k3_server_reduce<2><<<grid, kBlock, 0, s>>>(p); break;
+    case 4: k3_server_reduce<4><<<grid, kBlock, 0, s>>>(p); break;
+    case 8: k3_server_reduce<8><<<grid, kBlock, 0, s>>>(p); break;
+    default: k3_server_reduce<0><<<grid, kBlock, 0, s>>>(p); break;
+  }
+  return 1;
+}
+
+int launch_k5(const K5Params& p, int grid, cudaStream_t s) {
+  if (p.res_prev) k5_update_a<1><<<grid, kBlock, 0, s>>>(p);
+  else k5_update_a<0><<<grid, kBlock, 0, s>>>(p);
+  return 1;
+}
+
+int launch_epilogue(const EpiParams& p, cudaStream_t s) {
+  k_epilogue<<<p.L, 1024, 0, s>>>(p);
+  return 1;
+}
+
+int launch_k6(const K6Params& p, int grid, cudaStream_t s) {
+  k6_update_b<<<grid, kBlock, 0, s>>>(p);
+  return 1;
+}
+
+int launch_w1(const W1Params& p, int grid, cudaStream_t s) {
+  kw1_warmup_a<<<grid, kBlock, 0, s>>>(p);
+  return 1;
+}
+
+int launch_wepilogue(const WEpiParams& p, cudaStream_t s) {
+  k_wepilogue<<<p.L, 1024, 0, s>>>(p);
+  return 1;
+}
+
+int launch_w2(const W2Params& p, int grid, cudaStream_t s) {
+  kw2_warmup_b<<<grid, kBlock, 0, s>>>(p);
+  return 1;
+}
+
+int launch_average(const float* in, uint64_t stride, int n, uint64_t len, float* out,
+                   unsigned long long* err, int check_finite, int worker_base, cudaStream_t s) {
+  k_average<<<grid_for_elems(len), 256, 0, s>>>(in, stride, n, len, out, err, check_finite,
+                                                 worker_base);
+  return 1;
+}
+
+int launch_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
+                      uint64_t d, float* out, cudaStream_t s) {
+  k_decompress<<<grid_for_elems(d), 256, 0, s>>>(res, n, c, slot, W, d, out);
+  return 1;
+}
+
+int launch_materialize_error(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot,
+                             uint64_t W, uint64_t c, uint64_t len, float* out, cudaStream_t s) {
+  k_materialize_error<<<grid_for_elems(len), 256, 0, s>>>(raw, c_pad, pk, slot, W, c, len, out);
+  return 1;
+}
+
+int launch_materialize_m(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
+                         const uint64_t* off, int L, const float* invc, uint64_t d, float* out,
+                         cudaStream_t s) {
+  k_materialize_m<<<grid_for_elems(d), 256, 0, s>>>(res, n, c, slot, W, off, L, invc, d, out);
+  return 1;
+}
+
+int launch_error_stats(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot,
+                       uint64_t W, uint64_t c, uint64_t len, double* scratch, int scratch_tiles,
+                       float* scratch_max, double* out, cudaStream_t s) {
+  const int g = scratch_tiles / kWarpsPerBlock + 1;
+  k_error_stats_tiles<<<g < 148 * 8 ? g : 148 * 8, kBlock, 0, s>>>(
+      raw, c_pad, pk, slot, W, c, len, scratch, scratch_max, scratch_tiles);
+  k_error_stats_final<<<1, 1024, 0, s>>>(scratch, scratch_max, scratch_tiles, out);
+  return 2;
+}
+
+int launch_set_float(float* p, float v, cudaStream_t s) {
+  k_set_float<<<1, 1, 0, s>>>(p, v);
+  return 1;
+}
+
+}  // namespace bl

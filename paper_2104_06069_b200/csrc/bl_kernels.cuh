@@ -1,0 +1,210 @@
+// bl_kernels.cuh — sm_100a kernels of the 1-bit LAMB compression-stage path.
+//
+// Every kernel streams flat fp32 buffers in "tiles" of 4096 elements
+// (32 rows x 128); one warp owns one tile, lane l owns elements 4l..4l+3 of
+// each row (128-bit accesses).  A tile never straddles its reduction segment:
+// chunk kernels (K1 worker compress, K3 server reduce) tile each chunk from its
+// own element 0, layer kernels (K5/K6 update, W1/W2 warmup) tile each layer
+// from its own element 0.  This fixes the reduction order of every sum
+// ("tile-tree") independently of the launch shape, which is what
+// oracle/liboracle_f32.so restates bit-for-bit.
+#pragma once
+
+#include <cstdint>
+
+namespace bl {
+
+constexpr int kTile = 4096;  // elements per tile
+constexpr int kRowElems = 128;
+constexpr int kRowsPerTile = 32;
+constexpr int kWarpsPerBlock = 8;
+constexpr int kBlock = 256;
+
+// Device error words (atomicMin keys, ~0ull = none).
+enum ErrSlot : int {
+  kErrGrad = 0,    // non-finite gradient: key = worker << 40 | element
+  kErrScale = 1,   // non-finite compression scale: key = endpoint id
+  kErrRecon = 2,   // non-finite reconstructed gradient: key = layer
+  kErrSlots = 4,
+};
+
+// K1: worker compression of `nw` local streams, each split into n chunks.
+struct K1Params {
+  int n;             // chunks per stream (world size)
+  int nw;            // local workers (sim: n, nccl: 1)
+  int tpc;           // tiles per chunk
+  int L;             // layers (stream modes 1/2)
+  uint64_t c;        // chunk length
+  uint64_t c_pad;    // chunk stride of werr (multiple of 4096)
+  uint64_t d;        // fused length; elements >= d are zero padding
+  uint64_t slot;     // words per packet slot (W + 32), W = c_pad / 32
+  uint64_t W;
+  const float* in;   // mode 0: streams; modes 1/2: gradients; [nw][in_stride]
+  uint64_t in_stride;
+  const float* m;             // mode 1: momentum buffer
+  const uint32_t* res_prev;   // mode 2: previous result packets [n][slot]
+  const uint64_t* off;        // layer offsets [L+1]
+  const float* A;             // coeff*beta1 (fp32)
+  const float* B;             // coeff*(1-beta1)
+  const float* invc;          // 1/coeff
+  const float* es_dev;        // error scale (device scalar) or nullptr
+  float es_host;
+  float* werr;                // [nw][n][c_pad] raw residual (v + delta)
+  uint32_t* pk_cur;           // [nw][n][slot]
+  const uint32_t* pk_prev;    // [nw][n][slot]
+  double* partials;           // [nw][n][tpc]
+  float* cmax;                // [nw][n][tpc] max|corrected| per tile (stats) or nullptr
+  unsigned long long* err;
+  int worker_base;            // global worker id of local worker 0
+};
+
+// K3: server reduction of chunk(s) owned locally.
+struct K3Params {
+  int n;              // workers feeding each server
+  int ns;             // local servers (sim: n, nccl: 1)
+  int tpc;
+  int server_base;    // chunk id of local server 0
+  uint64_t c, c_pad, slot, W;
+  const uint32_t* in;         // worker packets: server s, worker i at in + s*in_s + i*in_i
+  uint64_t in_s, in_i;
+  float* serr;                // [ns][c_pad]
+  const uint32_t* res_prev;   // [n][slot]
+  uint32_t* res_cur;          // [n][slot]
+  const float* es_dev;
+  float es_host;
+  double* partials;           // [ns][tpc]
+  float* cmax;                // [ns][tpc] or nullptr
+};
+
+struct FinalizeParams {
+  const double* partials;  // [count][tpc]
+  int tpc;
+  uint64_t c;
+  uint32_t* slots;         // scale word of endpoint e at slots + e*slot_stride + W
+  uint64_t slot_stride, W;
+  unsigned long long* err;
+  int err_base;            // key offset for kErrScale
+};
+
+// Layer-tiled kernels (K5, K6, W1, W2).
+struct LayerTiles {
+  int L;
+  int tiles;                    // total tiles over all layers
+  const uint64_t* off;          // [L+1]
+  const int* tile_layer;        // [tiles]
+  const int* layer_tile_start;  // [L+1]
+};
+
+struct K5Params {
+  LayerTiles lt;
+  int n;
+  uint64_t c, slot, W;
+  const uint32_t* res_cur;   // [n][slot]
+  const uint32_t* res_prev;  // [n][slot] (m_prev from packets) or nullptr
+  const float* m;            // m_prev buffer (first step after the freeze)
+  const float* invc;
+  float* v;
+  const float* vf;
+  float inv, ninvb, b2, omb2, floor_;
+  float* tile_max;           // [tiles]
+  double* tile_v2;           // [tiles]
+  unsigned long long* err;
+};
+
+struct EpiParams {
+  int L;
+  const int* layer_tile_start;
+  const float* tile_max;
+  const double* tile_v2;
+  double* r_prev;
+  const double* c_avg;
+  float* coef_x;            // -lr*c per layer (fp32)
+  double* trace;            // [4L]
+  double* cmean;            // [2]: c_mean_prev, c_mean_prev2
+  float* es_next;
+  unsigned int* counter;
+  double lr, r_thr, r_min, r_max, floor_;
+  int scaled_ef;
+};
+
+struct K6Params {
+  LayerTiles lt;
+  int n;
+  uint64_t c, slot, W;
+  const uint32_t* res_cur;
+  const float* invc;
+  const float* coef_x;
+  const float* vf;
+  float* x;
+  float eta, wd;
+};
+
+struct W1Params {
+  LayerTiles lt;
+  const float* gbar;
+  float *m, *v;
+  const float* x;
+  float b1, omb1, b2, omb2, eta, wd;
+  double* tile_sums;  // [tiles][4]: x^2, u^2, v^2, |m|
+  int adam;           // adam_step: no norms needed (kept for the trace)
+};
+
+struct WEpiParams {
+  int L;
+  const int* layer_tile_start;
+  const uint64_t* off;
+  const double* tile_sums;
+  double* c_avg;
+  float* coef_x;
+  double* trace;
+  double* mag;         // [L] floored mean |m| (finalize)
+  double* coeff;       // [L]
+  float *A, *B, *invc;
+  double* cmean;
+  float* es_next;
+  unsigned int* counter;
+  double lr, b1, b3, c_min, c_max, floor_;
+  int track, finalize, adam, onebit_adam;
+};
+
+struct W2Params {
+  LayerTiles lt;
+  const float *m, *v;
+  float* x;
+  float* vf;  // written when finalize
+  const float* coef_x;
+  float eta, wd;
+  int finalize;
+};
+
+// Host launchers (bl_kernels.cu).  Each returns the number of kernels launched.
+int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s);
+int launch_finalize(const FinalizeParams& p, int count, cudaStream_t s);
+int launch_k3(const K3Params& p, int grid, cudaStream_t s);
+int launch_k5(const K5Params& p, int grid, cudaStream_t s);
+int launch_epilogue(const EpiParams& p, cudaStream_t s);
+int launch_k6(const K6Params& p, int grid, cudaStream_t s);
+int launch_w1(const W1Params& p, int grid, cudaStream_t s);
+int launch_wepilogue(const WEpiParams& p, cudaStream_t s);
+int launch_w2(const W2Params& p, int grid, cudaStream_t s);
+// out[k] = (float)(sum_i in[i*stride + k] (double, ascending i) * inv_n), k < len.
+int launch_average(const float* in, uint64_t stride, int n, uint64_t len, float* out,
+                   unsigned long long* err, int check_finite, int worker_base, cudaStream_t s);
+// out[k] (k < d) = decompressed result of packets res[n][slot].
+int launch_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
+                      uint64_t d, float* out, cudaStream_t s);
+// out[k] (k < len) = raw[j][i] - (bit ? S : -S) for flat k = j*c + i; pk [nch][slot].
+int launch_materialize_error(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot,
+                             uint64_t W, uint64_t c, uint64_t len, float* out, cudaStream_t s);
+// out[k] (k < d) = decompressed result * invc[layer(k)].
+int launch_materialize_m(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
+                         const uint64_t* off, int L, const float* invc, uint64_t d, float* out,
+                         cudaStream_t s);
+// Endpoint statistics (comm_sim.cpp:108-118): out[0] = sum delta^2 (tile-tree
+// over the flat residual), out[1] = max|delta|.
+int launch_error_stats(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot,
+                       uint64_t W, uint64_t c, uint64_t len, double* scratch, int scratch_tiles,
+                       float* scratch_max, double* out, cudaStream_t s);
+int launch_set_float(float* p, float v, cudaStream_t s);
+
+}  // namespace bl

@@ -1,0 +1,1177 @@
+// bl_runtime.cu — host runtime of the B200 1-bit LAMB path: the cluster
+// (communicator + residuals + packets) and the optimizer (layer state), and
+// the extern "C" ABI declared in include/bitlamb_b200.h.
+//
+// Step schedule of one compression-stage step (optimizers.cpp:231-332) on one
+// stream:  K1 worker compress -> scale finalize -> [NCCL alltoall of packets]
+// -> K3 server reduce -> scale finalize -> [NCCL allgather of server packets]
+// -> K5 (v, ratio max) -> per-layer epilogue -> K6 (x).  SIM mode runs the n
+// ranks' K1/K3 work in the same launches and skips the two exchanges.
+
+#include "bl_runtime.h"
+
+#include <algorithm>
+#include <cinttypes>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+namespace bl {
+
+const char* const kClassNames[KC_COUNT] = {
+    "k1_worker_compress", "finalize_scales", "k3_server_reduce", "k5_update_a",
+    "layer_epilogue",     "k6_update_b",     "w1_warmup_a",      "warmup_epilogue",
+    "w2_warmup_b",        "average",         "decompress",       "materialize",
+    "endpoint_stats",     "nccl_alltoall",   "nccl_allgather",   "h2d_copy",
+    "d2h_copy"};
+
+void fail(bl_status st, const std::string& msg) { throw Error{st, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(BL_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(BL_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+DeviceGuard::DeviceGuard(int dev) : dev_(dev) {
+  cudaGetDevice(&prev_);
+  if (prev_ != dev_) cuda_check(cudaSetDevice(dev_), "cudaSetDevice");
+}
+DeviceGuard::~DeviceGuard() {
+  if (prev_ >= 0 && prev_ != dev_) cudaSetDevice(prev_);
+}
+
+template <typename T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+  cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+  cuda_check(cudaMemset(p, 0, bytes), "cudaMemset");
+  return static_cast<T*>(p);
+}
+template float* dalloc<float>(size_t);
+template double* dalloc<double>(size_t);
+template uint32_t* dalloc<uint32_t>(size_t);
+
+static uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+
+// Slack after every streamed buffer: the row loader reads up to 132 floats
+// past a row start and rows may start up to 4095 floats before the end.
+constexpr uint64_t kSlack = 4096 + 256;
+
+}  // namespace bl
+
+using namespace bl;
+
+// ---------------------------------------------------------------------------
+// bl_cluster
+// ---------------------------------------------------------------------------
+cudaEvent_t bl_cluster::get_event() {
+  if (!ev_pool.empty()) {
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+void bl_cluster::begin(int, cudaEvent_t* a) {
+  *a = nullptr;
+  if (profiling) {
+    *a = get_event();
+    cuda_check(cudaEventRecord(*a, stream), "cudaEventRecord");
+  }
+}
+
+void bl_cluster::end(int cls, cudaEvent_t a, int kernels) {
+  launches += static_cast<uint64_t>(kernels);
+  if (kernels > 0) cuda_check(cudaGetLastError(), kClassNames[cls]);
+  if (profiling && a) {
+    cudaEvent_t b = get_event();
+    cuda_check(cudaEventRecord(b, stream), "cudaEventRecord");
+    pending.push_back({cls, a, b});
+  }
+}
+
+int bl_cluster::grid(long long tiles) const {
+  const long long want = (tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const long long cap = static_cast<long long>(sms) * 8;
+  return static_cast<int>(std::max<long long>(1, std::min(want, cap)));
+}
+
+uint64_t bl_cluster::chunk_payload_bits(uint64_t j) const {  // comm_sim.cpp:68-79
+  const uint64_t begin = j * c;
+  if (begin >= dim) return 0;
+  const uint64_t real = std::min(c, dim - begin);
+  if (cfg.compressor == BL_COMPRESSOR_ONEBIT) return real + 32;
+  return real * static_cast<uint64_t>(cfg.baseline_bits_per_element);
+}
+
+void bl_cluster::ledger_compressed() {  // comm_sim.cpp:187-197
+  uint64_t bits = 0;
+  for (int j = 0; j < n; ++j) bits += chunk_payload_bits(static_cast<uint64_t>(j));
+  ledger.gather_bits += static_cast<uint64_t>(n - 1) * bits;
+  ledger.scatter_bits += static_cast<uint64_t>(n - 1) * bits;
+  ledger.baseline_equivalent_bits += 2ull * static_cast<uint64_t>(n - 1) * dim *
+                                     static_cast<uint64_t>(cfg.baseline_bits_per_element);
+  ledger.compressed_collectives += 1;
+}
+
+void bl_cluster::ledger_lossless() {  // comm_sim.cpp:224-231
+  const uint64_t bits = 2ull * static_cast<uint64_t>(n - 1) * dim *
+                        static_cast<uint64_t>(cfg.baseline_bits_per_element);
+  ledger.lossless_bits += bits;
+  ledger.baseline_equivalent_bits += bits;
+  ledger.lossless_collectives += 1;
+}
+
+void bl_cluster::copy_inputs(const float* const* inputs, int n_inputs, uint64_t len, int memory) {
+  cudaEvent_t a;
+  begin(KC_H2D, &a);
+  for (int w = 0; w < n_inputs; ++w) {
+    float* dst = in + static_cast<size_t>(w) * in_stride;
+    if (memory == BL_MEM_DEVICE && inputs[w] == dst) continue;
+    cuda_check(cudaMemcpyAsync(dst, inputs[w], len * sizeof(float), cudaMemcpyDefault, stream),
+               "cudaMemcpyAsync(inputs)");
+  }
+  end(KC_H2D, a, 0);
+}
+
+void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, const float* es_dev) {
+  K1Params p = ovr ? *ovr : K1Params{};
+  p.n = n;
+  p.nw = nw;
+  p.tpc = tpc;
+  p.c = c;
+  p.c_pad = c_pad;
+  p.d = dim;
+  p.slot = slot;
+  p.W = W;
+  p.in = in;
+  p.in_stride = in_stride;
+  p.es_dev = es_dev;
+  p.es_host = es_host;
+  p.werr = werr;
+  p.pk_cur = wpk[cur()];
+  p.pk_prev = wpk[prev()];
+  p.partials = wpart;
+  p.cmax = cfg.endpoint_stats ? wcmax : nullptr;
+  p.err = err;
+  p.worker_base = mode == BL_MODE_SIM ? 0 : rank;
+  cudaEvent_t a;
+  begin(KC_K1, &a);
+  end(KC_K1, a, launch_k1(p, k1_mode, grid(static_cast<long long>(nw) * n * tpc), stream));
+
+  FinalizeParams f{wpart, tpc, c, wpk[cur()], slot, W, err, p.worker_base * n};
+  begin(KC_FIN, &a);
+  end(KC_FIN, a, launch_finalize(f, nw * n, stream));
+
+  const uint32_t* kin = wpk[cur()];
+  uint64_t in_s = slot, in_i = static_cast<uint64_t>(n) * slot;
+  if (mode == BL_MODE_NCCL) {
+    begin(KC_A2A, &a);
+    const size_t words = W + 1;  // sign words + scale word
+    cuda_check(cudaMemcpyAsync(rpk + static_cast<size_t>(rank) * slot,
+                               wpk[cur()] + static_cast<size_t>(rank) * slot, words * 4,
+                               cudaMemcpyDeviceToDevice, stream),
+               "self packet copy");
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (int j = 0; j < n; ++j) {
+      if (j == rank) continue;
+      nccl_check(ncclSend(wpk[cur()] + static_cast<size_t>(j) * slot, words, ncclUint32, j, comm,
+                          stream),
+                 "ncclSend");
+      nccl_check(ncclRecv(rpk + static_cast<size_t>(j) * slot, words, ncclUint32, j, comm, stream),
+                 "ncclRecv");
+    }
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    end(KC_A2A, a, 0);
+    kin = rpk;
+    in_s = 0;
+    in_i = slot;
+  }
+
+  K3Params k3{};
+  k3.n = n;
+  k3.ns = ns;
+  k3.tpc = tpc;
+  k3.server_base = mode == BL_MODE_SIM ? 0 : rank;
+  k3.c = c;
+  k3.c_pad = c_pad;
+  k3.slot = slot;
+  k3.W = W;
+  k3.in = kin;
+  k3.in_s = in_s;
+  k3.in_i = in_i;
+  k3.serr = serr;
+  k3.res_prev = res[prev()];
+  k3.res_cur = res[cur()];
+  k3.es_dev = es_dev;
+  k3.es_host = es_host;
+  k3.partials = spart;
+  k3.cmax = cfg.endpoint_stats ? scmax : nullptr;
+  begin(KC_K3, &a);
+  end(KC_K3, a, launch_k3(k3, grid(static_cast<long long>(ns) * tpc), stream));
+
+  FinalizeParams f2{spart, tpc, c, res[cur()] + static_cast<size_t>(k3.server_base) * slot, slot,
+                    W, err, 1 << 20};
+  begin(KC_FIN, &a);
+  end(KC_FIN, a, launch_finalize(f2, ns, stream));
+
+  if (mode == BL_MODE_NCCL && n > 1) {
+    begin(KC_AG, &a);
+    nccl_check(ncclAllGather(res[cur()] + static_cast<size_t>(rank) * slot, res[cur()], slot,
+                             ncclUint32, comm, stream),
+               "ncclAllGather");
+    end(KC_AG, a, 0);
+  }
+  calls += 1;
+  last_identity = false;
+  ledger_compressed();
+  if (cfg.endpoint_stats) refresh_stats();
+}
+
+void bl_cluster::lossless(bool check_finite) {
+  cudaEvent_t a;
+  if (mode == BL_MODE_SIM || n == 1) {
+    begin(KC_AVG, &a);
+    end(KC_AVG, a, launch_average(in, in_stride, nw, dim, out, err, check_finite ? 1 : 0,
+                                  mode == BL_MODE_SIM ? 0 : rank, stream));
+    return;
+  }
+  // Deterministic all-reduce: alltoall of fp32 chunks, ascending-rank fp64
+  // average of the own chunk, allgather (same bytes as a ring RS + AG).
+  begin(KC_A2A, &a);
+  cuda_check(cudaMemcpyAsync(lrecv + static_cast<size_t>(rank) * c_pad,
+                             in + static_cast<size_t>(rank) * c, c * sizeof(float),
+                             cudaMemcpyDeviceToDevice, stream),
+             "self chunk copy");
+  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  for (int j = 0; j < n; ++j) {
+    if (j == rank) continue;
+    nccl_check(ncclSend(in + static_cast<size_t>(j) * c, c, ncclFloat32, j, comm, stream), "ncclSend");
+    nccl_check(ncclRecv(lrecv + static_cast<size_t>(j) * c_pad, c, ncclFloat32, j, comm, stream),
+               "ncclRecv");
+  }
+  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  end(KC_A2A, a, 0);
+  if (check_finite) {
+    // check_gradients covers the rank's whole gradient, not just its chunk.
+    begin(KC_AVG, &a);
+    end(KC_AVG, a, launch_average(in, in_stride, 1, dim, nullptr, err, 1, rank, stream));
+  }
+  begin(KC_AVG, &a);
+  end(KC_AVG, a, launch_average(lrecv, c_pad, n, c, out + static_cast<size_t>(rank) * c, err, 0,
+                                0, stream));
+  begin(KC_AG, &a);
+  nccl_check(ncclAllGather(out + static_cast<size_t>(rank) * c, out, c, ncclFloat32, comm, stream),
+             "ncclAllGather");
+  end(KC_AG, a, 0);
+}
+
+void bl_cluster::refresh_stats() {  // comm_sim.cpp:108-118, 175-180
+  cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+  const int latest = static_cast<int>((calls + 1u) & 1u);
+  auto update = [](bl_endpoint_stats& s, double l2, double linf, double cinf) {
+    s.delta_l2 = l2;
+    s.delta_linf = linf;
+    s.corrected_linf = cinf;
+    s.max_delta_linf = std::max(s.max_delta_linf, linf);
+    s.max_corrected_linf = std::max(s.max_corrected_linf, cinf);
+  };
+  std::vector<float> cm(static_cast<size_t>(std::max(nw * n, ns)) * tpc);
+  double host[2];
+  for (int w = 0; w < nw; ++w) {
+    cudaEvent_t a;
+    begin(KC_STATS, &a);
+    end(KC_STATS, a,
+        launch_error_stats(werr + static_cast<size_t>(w) * n * c_pad, c_pad,
+                           wpk[latest] + static_cast<size_t>(w) * n * slot, slot, W, c, P,
+                           stat_part, stat_tiles, stat_max, stat_out, stream));
+    cuda_check(cudaMemcpyAsync(host, stat_out, sizeof host, cudaMemcpyDeviceToHost, stream), "stats");
+    cuda_check(cudaMemcpyAsync(cm.data(), wcmax + static_cast<size_t>(w) * n * tpc,
+                               static_cast<size_t>(n) * tpc * sizeof(float), cudaMemcpyDeviceToHost,
+                               stream),
+               "stats");
+    cuda_check(cudaStreamSynchronize(stream), "stats sync");
+    float cmax = 0.f;
+    for (int k = 0; k < n * tpc; ++k) cmax = cmax < cm[k] ? cm[k] : cmax;
+    const int gw = mode == BL_MODE_SIM ? w : rank;
+    update(stats[gw], std::sqrt(host[0]), host[1], cmax);
+  }
+  for (int s = 0; s < ns; ++s) {
+    const int j = mode == BL_MODE_SIM ? s : rank;
+    cudaEvent_t a;
+    begin(KC_STATS, &a);
+    end(KC_STATS, a,
+        launch_error_stats(serr + static_cast<size_t>(s) * c_pad, c_pad,
+                           res[latest] + static_cast<size_t>(j) * slot, slot, W, c, c, stat_part,
+                           stat_tiles, stat_max, stat_out, stream));
+    cuda_check(cudaMemcpyAsync(host, stat_out, sizeof host, cudaMemcpyDeviceToHost, stream), "stats");
+    cuda_check(cudaMemcpyAsync(cm.data(), scmax + static_cast<size_t>(s) * tpc,
+                               static_cast<size_t>(tpc) * sizeof(float), cudaMemcpyDeviceToHost,
+                               stream),
+               "stats");
+    cuda_check(cudaStreamSynchronize(stream), "stats sync");
+    float cmax = 0.f;
+    for (int k = 0; k < tpc; ++k) cmax = cmax < cm[k] ? cm[k] : cmax;
+    update(stats[n + j], std::sqrt(host[0]), host[1], cmax);
+  }
+}
+
+void bl_cluster::check_errors(const std::vector<uint64_t>* off) {
+  unsigned long long e[kErrSlots];
+  cuda_check(cudaMemcpy(e, err, sizeof e, cudaMemcpyDeviceToHost), "error words");
+  const unsigned long long none = ~0ull;
+  bool any = false;
+  for (int k = 0; k < kErrSlots; ++k) any |= e[k] != none;
+  if (!any) return;
+  cuda_check(cudaMemset(err, 0xFF, sizeof e), "reset error words");
+  char buf[256];
+  if (e[kErrGrad] != none) {  // optimizers.cpp:109-114
+    const unsigned long long w = e[kErrGrad] >> 40, k = e[kErrGrad] & ((1ull << 40) - 1);
+    long long layer = -1;
+    if (off) layer = std::upper_bound(off->begin(), off->end(), static_cast<uint64_t>(k)) - off->begin() - 1;
+    std::snprintf(buf, sizeof buf, "non-finite gradient at step %" PRIu64 ", worker %llu, layer 'layer%lld'",
+                  pending_step, w, layer);
+    fail(BL_ERR_RUNTIME, buf);
+  }
+  if (e[kErrScale] != none) fail(BL_ERR_INVALID_ARGUMENT, "compress: input vector is not finite");
+  if (e[kErrRecon] != none) {  // optimizers.cpp:288-293
+    std::snprintf(buf, sizeof buf, "non-finite reconstructed gradient for layer 'layer%llu'",
+                  e[kErrRecon]);
+    fail(BL_ERR_RUNTIME, buf);
+  }
+}
+
+void bl_cluster::sync_and_check(const std::vector<uint64_t>* off) {
+  cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+  check_errors(off);
+}
+
+// ---------------------------------------------------------------------------
+// bl_optimizer
+// ---------------------------------------------------------------------------
+void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, bool adam) {
+  cl->lossless(true);  // average_lossless (optimizers.cpp:119-138)
+  cl->ledger_lossless();
+  cudaEvent_t a;
+  W1Params w1{};
+  w1.lt = lt();
+  w1.gbar = cl->out;
+  w1.m = m;
+  w1.v = v;
+  w1.x = x;
+  w1.b1 = static_cast<float>(hp.beta1);
+  w1.omb1 = static_cast<float>(1.0 - hp.beta1);
+  w1.b2 = static_cast<float>(hp.beta2);
+  w1.omb2 = static_cast<float>(1.0 - hp.beta2);
+  w1.eta = static_cast<float>(hp.eta);
+  w1.wd = static_cast<float>(hp.weight_decay);
+  w1.tile_sums = tile_sums;
+  w1.adam = adam ? 1 : 0;
+  cl->begin(KC_W1, &a);
+  cl->end(KC_W1, a, launch_w1(w1, cl->grid(tiles), cl->stream));
+
+  WEpiParams we{};
+  we.L = L;
+  we.layer_tile_start = layer_tile_start;
+  we.off = off_dev;
+  we.tile_sums = tile_sums;
+  we.c_avg = c_avg;
+  we.coef_x = coef_x;
+  we.trace = trace;
+  we.mag = mag;
+  we.coeff = coeff;
+  we.A = A;
+  we.B = B;
+  we.invc = invc;
+  we.cmean = cmean;
+  we.es_next = es;
+  we.counter = counter;
+  we.lr = lr;
+  we.b1 = hp.beta1;
+  we.b3 = hp.beta3;
+  we.c_min = hp.c_min;
+  we.c_max = hp.c_max;
+  we.floor_ = hp.division_floor;
+  we.track = track ? 1 : 0;
+  we.finalize = finalize ? 1 : 0;
+  we.adam = adam ? 1 : 0;
+  we.onebit_adam = variant == BL_ONEBIT_ADAM ? 1 : 0;
+  cl->begin(KC_WEPI, &a);
+  cl->end(KC_WEPI, a, launch_wepilogue(we, cl->stream));
+
+  W2Params w2{};
+  w2.lt = lt();
+  w2.m = m;
+  w2.v = v;
+  w2.x = x;
+  w2.vf = vf;
+  w2.coef_x = coef_x;
+  w2.eta = static_cast<float>(hp.eta);
+  w2.wd = static_cast<float>(hp.weight_decay);
+  w2.finalize = finalize ? 1 : 0;
+  cl->begin(KC_W2, &a);
+  cl->end(KC_W2, a, launch_w2(w2, cl->grid(tiles), cl->stream));
+}
+
+void bl_optimizer::compressed_step(double lr) {
+  if (cl->cfg.compressor != BL_COMPRESSOR_ONEBIT) {
+    fail(BL_ERR_UNSUPPORTED, "compressed step with the identity compressor is not on the B200 path");
+  }
+  if (variant != BL_ONEBIT_LAMB) {
+    fail(BL_ERR_UNSUPPORTED, "compression stage of this variant is not on the B200 path yet");
+  }
+  int mode = m_valid ? 1 : 2;
+  if (!m_valid && cl->calls != my_calls) {
+    fail(BL_ERR_LOGIC,
+         "momentum is encoded by the cluster's last result packets, but the cluster ran another "
+         "collective since the last optimizer step");
+  }
+  K1Params p{};
+  p.L = L;
+  p.m = m;
+  p.res_prev = cl->res[cl->prev()];  // latest result before this collective
+  p.off = off_dev;
+  p.A = A;
+  p.B = B;
+  p.invc = invc;
+  cl->compressed(&p, mode, 1.0f, es);
+
+  const int latest = static_cast<int>((cl->calls + 1u) & 1u);
+  const int before = static_cast<int>(cl->calls & 1u);
+  cudaEvent_t a;
+  K5Params k5{};
+  k5.lt = lt();
+  k5.n = cl->n;
+  k5.c = cl->c;
+  k5.slot = cl->slot;
+  k5.W = cl->W;
+  k5.res_cur = cl->res[latest];
+  const bool mprev_buf = m_valid || mprev_separate;
+  k5.res_prev = mprev_buf ? nullptr : cl->res[before];
+  k5.m = mprev_separate ? mprev : m;
+  k5.invc = invc;
+  k5.v = v;
+  k5.vf = vf;
+  const double inv = 1.0 / (1.0 - hp.beta1);
+  k5.inv = static_cast<float>(inv);
+  k5.ninvb = static_cast<float>(-hp.beta1 * inv);
+  k5.b2 = static_cast<float>(hp.beta2);
+  k5.omb2 = static_cast<float>(1.0 - hp.beta2);
+  k5.floor_ = static_cast<float>(hp.division_floor);
+  k5.tile_max = tile_max;
+  k5.tile_v2 = tile_sums;
+  k5.err = cl->err;
+  cl->begin(KC_K5, &a);
+  cl->end(KC_K5, a, launch_k5(k5, cl->grid(tiles), cl->stream));
+
+  EpiParams ep{};
+  ep.L = L;
+  ep.layer_tile_start = layer_tile_start;
+  ep.tile_max = tile_max;
+  ep.tile_v2 = tile_sums;
+  ep.r_prev = r_prev;
+  ep.c_avg = c_avg;
+  ep.coef_x = coef_x;
+  ep.trace = trace;
+  ep.cmean = cmean;
+  ep.es_next = es;
+  ep.counter = counter;
+  ep.lr = lr;
+  ep.r_thr = hp.r_threshold;
+  ep.r_min = hp.r_min;
+  ep.r_max = hp.r_max;
+  ep.floor_ = hp.division_floor;
+  ep.scaled_ef = hp.scaled_error_feedback;
+  cl->begin(KC_EPI, &a);
+  cl->end(KC_EPI, a, launch_epilogue(ep, cl->stream));
+
+  K6Params k6{};
+  k6.lt = lt();
+  k6.n = cl->n;
+  k6.c = cl->c;
+  k6.slot = cl->slot;
+  k6.W = cl->W;
+  k6.res_cur = cl->res[latest];
+  k6.invc = invc;
+  k6.coef_x = coef_x;
+  k6.vf = vf;
+  k6.x = x;
+  k6.eta = static_cast<float>(hp.eta);
+  k6.wd = static_cast<float>(hp.weight_decay);
+  cl->begin(KC_K6, &a);
+  cl->end(KC_K6, a, launch_k6(k6, cl->grid(tiles), cl->stream));
+
+  m_valid = false;
+  mprev_separate = false;
+  my_calls = cl->calls;
+}
+
+void bl_optimizer::step(const float* const* grads, int n_grads, uint64_t t, double lr, int memory,
+                        bl_step_trace* tr) {
+  if (n_grads < 1) fail(BL_ERR_INVALID_ARGUMENT, "step: no worker gradients");
+  if (n_grads != cl->nw) {
+    fail(BL_ERR_DIMENSION, "step: worker count: size mismatch (" + std::to_string(n_grads) +
+                               " vs " + std::to_string(cl->nw) + ")");
+  }
+  const bool two = two_stage();
+  const bool adam = variant == BL_ADAM || variant == BL_ONEBIT_ADAM;
+  bool compressed = false;
+  if (!two || t < hp.warmup_steps) {
+    cl->copy_inputs(grads, n_grads, d, memory);
+    const bool finalize = two && t + 1 == hp.warmup_steps;
+    warmup_step(t, lr, two && !adam, finalize, adam);
+    if (finalize) {  // optimizers.cpp:202-224
+      frozen = true;
+      has_vf = true;
+      if (variant == BL_ONEBIT_LAMB) has_mprev = true;
+      m_valid = true;
+    }
+  } else {
+    if (!frozen) {
+      fail(BL_ERR_STAGE_ORDER,
+           "compression-stage step before warmup finalized: frozen variance, c_avg and momentum "
+           "snapshot are missing");
+    }
+    cl->copy_inputs(grads, n_grads, d, memory);
+    compressed_step(lr);
+    compressed = true;
+  }
+  cl->pending_step = t;
+  cl->pending_is_step = true;
+  if (tr) {
+    std::vector<double> h(4 * static_cast<size_t>(L));
+    cudaEvent_t a;
+    cl->begin(KC_D2H, &a);
+    cuda_check(cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                               cl->stream),
+               "trace copy");
+    cl->end(KC_D2H, a, 0);
+    cl->sync_and_check(&off);
+    for (int l = 0; l < L; ++l) {
+      if (tr->c) tr->c[l] = h[l];
+      if (tr->r) tr->r[l] = h[L + l];
+      if (tr->v_norm) tr->v_norm[l] = h[2 * L + l];
+      if (tr->v_ratio_preclip) tr->v_ratio_preclip[l] = h[3 * L + l];
+    }
+    tr->compressed = compressed ? 1 : 0;
+  }
+}
+
+void bl_optimizer::materialize_m(float* dst) {
+  const int latest = static_cast<int>((cl->calls + 1u) & 1u);
+  cudaEvent_t a;
+  cl->begin(KC_MAT, &a);
+  cl->end(KC_MAT, a,
+          launch_materialize_m(cl->res[latest], cl->n, cl->c, cl->slot, cl->W, off_dev, L, invc, d,
+                               dst, cl->stream));
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+bl_status guarded(F&& f) {
+  try {
+    f();
+    return BL_OK;
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.status;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return BL_ERR_RUNTIME;
+  }
+}
+
+void check_arg(bool ok, const char* msg) {
+  if (!ok) fail(BL_ERR_INVALID_ARGUMENT, msg);
+}
+
+void size_check(uint64_t a, uint64_t b, const char* what) {  // errors.hpp:43-48
+  if (a != b) {
+    fail(BL_ERR_DIMENSION, std::string(what) + ": size mismatch (" + std::to_string(a) + " vs " +
+                               std::to_string(b) + ")");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bl_last_error(void) { return g_err.c_str(); }
+int32_t bl_abi_version(void) { return BL_ABI_VERSION; }
+
+bl_status bl_nccl_get_unique_id(uint8_t* out) {
+  return guarded([&] {
+    ncclUniqueId id;
+    nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id.internal) == BL_NCCL_UNIQUE_ID_BYTES, "unique id size");
+    std::memcpy(out, id.internal, BL_NCCL_UNIQUE_ID_BYTES);
+  });
+}
+
+void bl_hparams_default(bl_hparams* hp) {
+  *hp = bl_hparams{};
+  hp->beta1 = 0.9;
+  hp->beta2 = 0.999;
+  hp->beta3 = 0.9;
+  hp->eta = 1e-6;
+  hp->c_min = 0.01;
+  hp->c_max = 0.3;
+  hp->r_min = 0.5;
+  hp->r_max = 4.0;
+  hp->r_threshold = 0.1;
+  hp->weight_decay = 0.0;
+  hp->division_floor = 1e-12;
+}
+
+bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
+  return guarded([&] {
+    *out = nullptr;
+    check_arg(cfg->n_workers >= 1, "SimCluster: need at least one worker");
+    check_arg(cfg->dim >= 1, "SimCluster: dim must be >= 1");
+    check_arg(cfg->baseline_bits_per_element >= 1, "SimCluster: baseline bits must be >= 1");
+    if (cfg->verify_compensation) {
+      fail(BL_ERR_UNSUPPORTED,
+           "verify_compensation: the fp32 path checks the compensation identity in its test "
+           "suite, not per element at run time");
+    }
+    if (cfg->n_workers > 64) fail(BL_ERR_UNSUPPORTED, "more than 64 workers");
+    if (cfg->mode == BL_MODE_NCCL) {
+      check_arg(cfg->rank >= 0 && cfg->rank < cfg->n_workers, "rank out of range");
+      check_arg(cfg->nccl_unique_id != nullptr, "NCCL mode needs a unique id");
+    }
+    int ndev = 0;
+    cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (ndev == 0) fail(BL_ERR_CUDA, "no CUDA device");
+    check_arg(cfg->device >= 0 && cfg->device < ndev, "device ordinal out of range");
+    DeviceGuard g(cfg->device);
+    auto* c = new bl_cluster();
+    try {
+      c->cfg = *cfg;
+      c->n = cfg->n_workers;
+      c->mode = cfg->mode;
+      c->rank = cfg->mode == BL_MODE_NCCL ? cfg->rank : 0;
+      c->device = cfg->device;
+      c->dim = cfg->dim;
+      c->P = (c->dim + c->n - 1) / c->n * c->n;  // comm_sim.cpp:58-59
+      c->c = c->P / c->n;
+      c->c_pad = round_up(c->c, kTile);
+      c->W = c->c_pad / 32;
+      c->slot = c->W + 32;
+      c->tpc = static_cast<int>(c->c_pad / kTile);
+      c->nw = c->mode == BL_MODE_SIM ? c->n : 1;
+      c->ns = c->nw;
+      c->in_stride = round_up(c->P + kSlack, 64);
+      cudaDeviceProp prop;
+      cuda_check(cudaGetDeviceProperties(&prop, cfg->device), "cudaGetDeviceProperties");
+      c->sms = prop.multiProcessorCount;
+      if (cfg->stream) {
+        c->stream = static_cast<cudaStream_t>(cfg->stream);
+      } else {
+        cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        c->own_stream = true;
+      }
+      const size_t nw = static_cast<size_t>(c->nw), n = static_cast<size_t>(c->n);
+      c->in = dalloc<float>(nw * c->in_stride);
+      c->werr = dalloc<float>(nw * n * c->c_pad + 256);
+      c->wpk[0] = dalloc<uint32_t>(nw * n * c->slot);
+      c->wpk[1] = dalloc<uint32_t>(nw * n * c->slot);
+      c->serr = dalloc<float>(static_cast<size_t>(c->ns) * c->c_pad + 256);
+      c->res[0] = dalloc<uint32_t>(n * c->slot);
+      c->res[1] = dalloc<uint32_t>(n * c->slot);
+      c->wpart = dalloc<double>(nw * n * c->tpc);
+      c->spart = dalloc<double>(static_cast<size_t>(c->ns) * c->tpc);
+      c->out = dalloc<float>(c->P + kSlack);
+      c->err = reinterpret_cast<unsigned long long*>(dalloc<double>(kErrSlots));
+      cuda_check(cudaMemset(c->err, 0xFF, kErrSlots * sizeof(unsigned long long)), "err init");
+      if (cfg->endpoint_stats) {
+        c->wcmax = dalloc<float>(nw * n * c->tpc);
+        c->scmax = dalloc<float>(static_cast<size_t>(c->ns) * c->tpc);
+        c->stat_tiles = static_cast<int>((c->P + kTile - 1) / kTile);
+        c->stat_part = dalloc<double>(c->stat_tiles);
+        c->stat_max = dalloc<float>(c->stat_tiles);
+        c->stat_out = dalloc<double>(2);
+      }
+      c->stats.assign(2 * n, bl_endpoint_stats{});
+      if (c->mode == BL_MODE_NCCL) {
+        c->rpk = dalloc<uint32_t>(n * c->slot);
+        c->lrecv = dalloc<float>(n * c->c_pad + kSlack);
+        ncclUniqueId id;
+        std::memcpy(id.internal, cfg->nccl_unique_id, BL_NCCL_UNIQUE_ID_BYTES);
+        nccl_check(ncclCommInitRank(&c->comm, c->n, id, c->rank), "ncclCommInitRank");
+      }
+      cuda_check(cudaDeviceSynchronize(), "cluster init");
+    } catch (...) {
+      bl_cluster_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void bl_cluster_destroy(bl_cluster* c) {
+  if (!c) return;
+  DeviceGuard g(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  void* bufs[] = {c->in,    c->werr,  c->wpk[0], c->wpk[1],    c->rpk,      c->serr,
+                  c->res[0], c->res[1], c->wpart, c->spart,    c->wcmax,    c->scmax,
+                  c->out,   c->lrecv, c->err,    c->stat_part, c->stat_max, c->stat_out};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  for (auto& e : c->pending) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+bl_status bl_cluster_dims(const bl_cluster* c, uint64_t* padded, uint64_t* chunk) {
+  return guarded([&] {
+    if (padded) *padded = c->P;
+    if (chunk) *chunk = c->c;
+  });
+}
+
+bl_status bl_cluster_compressed_allreduce(bl_cluster* c, const float* const* inputs,
+                                          int32_t n_inputs, uint64_t len, float* outp,
+                                          double error_scale, int32_t memory) {
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    size_check(static_cast<uint64_t>(n_inputs), static_cast<uint64_t>(c->nw),
+               "compressed_allreduce: worker count");
+    size_check(len, c->dim, "compressed_allreduce: input length");
+    c->copy_inputs(inputs, n_inputs, len, memory);
+    if (c->cfg.compressor == BL_COMPRESSOR_IDENTITY) {
+      // Identity compressor: lossless messages, residuals stay zero
+      // (compression.cpp:184-188), result = ascending-worker average.
+      c->lossless(false);
+      c->ledger_compressed();
+      c->last_identity = true;
+    } else {
+      c->compressed(nullptr, 0, static_cast<float>(error_scale), nullptr);
+      const int latest = static_cast<int>((c->calls + 1u) & 1u);
+      cudaEvent_t a;
+      c->begin(KC_DEC, &a);
+      c->end(KC_DEC, a, launch_decompress(c->res[latest], c->n, c->c, c->slot, c->W, c->dim, c->out,
+                                          c->stream));
+    }
+    c->pending_is_step = false;
+    if (outp) {
+      cuda_check(cudaMemcpyAsync(outp, c->out, c->dim * sizeof(float), cudaMemcpyDefault, c->stream),
+                 "result copy");
+      if (memory == BL_MEM_HOST) c->sync_and_check(nullptr);
+    }
+  });
+}
+
+bl_status bl_cluster_lossless_allreduce(bl_cluster* c, const float* const* inputs, int32_t n_inputs,
+                                        uint64_t len, float* outp, int32_t memory) {
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    size_check(static_cast<uint64_t>(n_inputs), static_cast<uint64_t>(c->nw),
+               "lossless_allreduce: worker count");
+    size_check(len, c->dim, "lossless_allreduce: input length");
+    c->copy_inputs(inputs, n_inputs, len, memory);
+    c->lossless(false);
+    c->ledger_lossless();
+    if (outp) {
+      cuda_check(cudaMemcpyAsync(outp, c->out, c->dim * sizeof(float), cudaMemcpyDefault, c->stream),
+                 "result copy");
+      if (memory == BL_MEM_HOST) c->sync_and_check(nullptr);
+    }
+  });
+}
+
+static void local_index(const bl_cluster* c, int32_t i, const char* what) {
+  if (i < 0 || i >= c->n) fail(BL_ERR_INVALID_ARGUMENT, std::string(what) + ": index out of range");
+  if (c->mode == BL_MODE_NCCL && i != c->rank) {
+    fail(BL_ERR_INVALID_ARGUMENT, std::string(what) + ": only the local rank's endpoint lives here");
+  }
+}
+
+bl_status bl_cluster_worker_error(bl_cluster* c, int32_t i, float* outp) {
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    local_index(c, i, "worker_error");
+    const int w = c->mode == BL_MODE_SIM ? i : 0;
+    c->sync_and_check(nullptr);
+    if (c->last_identity || c->calls == 0) {
+      std::memset(outp, 0, c->P * sizeof(float));
+      return;
+    }
+    const int latest = static_cast<int>((c->calls + 1u) & 1u);
+    float* tmp = c->out;  // scratch: P floats
+    cudaEvent_t a;
+    c->begin(KC_MAT, &a);
+    c->end(KC_MAT, a,
+           launch_materialize_error(c->werr + static_cast<size_t>(w) * c->n * c->c_pad, c->c_pad,
+                                    c->wpk[latest] + static_cast<size_t>(w) * c->n * c->slot,
+                                    c->slot, c->W, c->c, c->P, tmp, c->stream));
+    cuda_check(cudaMemcpyAsync(outp, tmp, c->P * sizeof(float), cudaMemcpyDeviceToHost, c->stream),
+               "worker_error copy");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+bl_status bl_cluster_server_error(bl_cluster* c, int32_t j, float* outp) {
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    local_index(c, j, "server_error");
+    const int s = c->mode == BL_MODE_SIM ? j : 0;
+    c->sync_and_check(nullptr);
+    if (c->last_identity || c->calls == 0) {
+      std::memset(outp, 0, c->c * sizeof(float));
+      return;
+    }
+    const int latest = static_cast<int>((c->calls + 1u) & 1u);
+    float* tmp = c->out;
+    cudaEvent_t a;
+    c->begin(KC_MAT, &a);
+    c->end(KC_MAT, a,
+           launch_materialize_error(c->serr + static_cast<size_t>(s) * c->c_pad, c->c_pad,
+                                    c->res[latest] + static_cast<size_t>(j) * c->slot, c->slot, c->W,
+                                    c->c, c->c, tmp, c->stream));
+    cuda_check(cudaMemcpyAsync(outp, tmp, c->c * sizeof(float), cudaMemcpyDeviceToHost, c->stream),
+               "server_error copy");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+static void packet_bytes(bl_cluster* c, const uint32_t* slot_ptr, uint8_t* bytes) {
+  const size_t nb = (c->c + 7) / 8;
+  std::vector<uint32_t> words(c->W + 1);
+  cuda_check(cudaMemcpyAsync(words.data(), slot_ptr, (c->W + 1) * 4, cudaMemcpyDeviceToHost,
+                             c->stream),
+             "packet copy");
+  cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  std::memcpy(bytes, words.data(), nb);  // LE words == LSB-first bytes
+  std::memcpy(bytes + nb, &words[c->W], 4);
+}
+
+bl_status bl_cluster_packet(bl_cluster* c, int32_t worker, int32_t server, uint8_t* bytes) {
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    local_index(c, worker, "packet");
+    if (server < 0 || server >= c->n) fail(BL_ERR_INVALID_ARGUMENT, "packet: server out of range");
+    if (c->last_identity) fail(BL_ERR_LOGIC, "identity packet");
+    const int w = c->mode == BL_MODE_SIM ? worker : 0;
+    const int latest = static_cast<int>((c->calls + 1u) & 1u);
+    packet_bytes(c, c->wpk[latest] + (static_cast<size_t>(w) * c->n + server) * c->slot, bytes);
+  });
+}
+
+bl_status bl_cluster_server_packet(bl_cluster* c, int32_t server, uint8_t* bytes) {
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    if (server < 0 || server >= c->n) fail(BL_ERR_INVALID_ARGUMENT, "packet: server out of range");
+    if (c->last_identity) fail(BL_ERR_LOGIC, "identity packet");
+    const int latest = static_cast<int>((c->calls + 1u) & 1u);
+    packet_bytes(c, c->res[latest] + static_cast<size_t>(server) * c->slot, bytes);
+  });
+}
+
+bl_status bl_cluster_ledger(const bl_cluster* c, bl_volume_ledger* outp) {
+  return guarded([&] { *outp = c->ledger; });
+}
+
+bl_status bl_cluster_stats(bl_cluster* c, bl_endpoint_stats* outp) {
+  return guarded([&] {
+    if (!c->cfg.endpoint_stats) fail(BL_ERR_LOGIC, "endpoint statistics are disabled in the config");
+    for (size_t k = 0; k < c->stats.size(); ++k) outp[k] = c->stats[k];
+  });
+}
+
+bl_status bl_cluster_synchronize(bl_cluster* c) {
+  return guarded([&] {
+    DeviceGuard g(c->device);
+    c->sync_and_check(nullptr);
+  });
+}
+
+float* bl_cluster_input_buffer(bl_cluster* c, int32_t worker) {
+  if (!c || worker < 0 || worker >= c->nw) return nullptr;
+  return c->in + static_cast<size_t>(worker) * c->in_stride;
+}
+
+uint64_t bl_cluster_kernel_launches(const bl_cluster* c) { return c ? c->launches : 0; }
+
+bl_status bl_cluster_set_profiling(bl_cluster* c, int32_t on) {
+  return guarded([&] {
+    c->profiling = on != 0;
+    for (int k = 0; k < KC_COUNT; ++k) {
+      c->prof_ms[k] = 0.0;
+      c->prof_n[k] = 0;
+    }
+  });
+}
+
+int32_t bl_cluster_profile(bl_cluster* c, const char** names, double* total_ms, uint64_t* launches,
+                           int32_t cap) {
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& e : c->pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    c->prof_ms[e.cls] += ms;
+    c->prof_n[e.cls] += 1;
+    c->ev_pool.push_back(e.a);
+    c->ev_pool.push_back(e.b);
+  }
+  c->pending.clear();
+  int k = 0;
+  for (int cls = 0; cls < KC_COUNT && k < cap; ++cls) {
+    if (c->prof_n[cls] == 0) continue;
+    names[k] = kClassNames[cls];
+    total_ms[k] = c->prof_ms[cls];
+    launches[k] = c->prof_n[cls];
+    ++k;
+  }
+  return k;
+}
+
+bl_status bl_volume_reduction(double w, double bb, double cb, double* outp) {
+  return guarded([&] {  // comm_sim.cpp:36-48
+    check_arg(w >= 0.0 && w <= 1.0, "volume_reduction: warmup_ratio must be in [0, 1]");
+    check_arg(bb > 0.0, "volume_reduction: baseline_bits must be > 0");
+    check_arg(cb >= 0.0, "volume_reduction: compressed bits must be >= 0");
+    const double denom = w + (1.0 - w) * cb / bb;
+    *outp = denom == 0.0 ? INFINITY : 1.0 / denom;
+  });
+}
+
+// HyperParams::validate, optimizers.cpp:60-74
+static void validate(const bl_hparams* h) {
+  auto reject = [](const char* m) { fail(BL_ERR_CONFIG, m); };
+  if (!(h->beta1 >= 0.0 && h->beta1 < 1.0)) reject("beta1 must be in [0, 1)");
+  if (!(h->beta2 >= 0.0 && h->beta2 < 1.0)) reject("beta2 must be in [0, 1)");
+  if (!(h->beta3 >= 0.0 && h->beta3 < 1.0)) reject("beta3 must be in [0, 1)");
+  if (!(h->eta > 0.0)) reject("eta must be > 0");
+  if (!(h->c_min <= h->c_max)) reject("c_min must not exceed c_max");
+  if (!(h->r_min <= h->r_max)) reject("r_min must not exceed r_max");
+  if (!(h->r_threshold > 0.0 && h->r_threshold < 1.0)) reject("r_threshold must be in (0, 1)");
+  if (!(h->weight_decay >= 0.0)) reject("weight_decay must be >= 0");
+  if (!(h->division_floor > 0.0)) reject("division_floor must be > 0");
+  if (h->warmup_steps > h->total_steps) reject("warmup_steps must not exceed total_steps");
+}
+
+bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_layers,
+                              const bl_hparams* hp, bl_cluster* cl, bl_optimizer** out) {
+  return guarded([&] {
+    *out = nullptr;
+    validate(hp);
+    check_arg(n_layers >= 1, "Optimizer: need at least one layer");
+    for (int l = 0; l < n_layers; ++l) check_arg(sizes[l] > 0, "Optimizer: layer size must be > 0");
+    check_arg(variant >= BL_LAMB && variant <= BL_ONEBIT_ADAM, "unknown optimizer variant");
+    check_arg(cl != nullptr, "Optimizer: needs the cluster whose device and stream it uses");
+    DeviceGuard g(cl->device);
+    auto* o = new bl_optimizer();
+    try {
+      o->variant = variant;
+      o->L = n_layers;
+      o->hp = *hp;
+      o->cl = cl;
+      o->off.assign(static_cast<size_t>(n_layers) + 1, 0);
+      std::vector<int> tstart(static_cast<size_t>(n_layers) + 1, 0);
+      for (int l = 0; l < n_layers; ++l) {
+        o->off[l + 1] = o->off[l] + sizes[l];
+        tstart[l + 1] = tstart[l] + static_cast<int>((sizes[l] + kTile - 1) / kTile);
+      }
+      o->d = o->off[n_layers];
+      if (o->d != cl->dim) {
+        fail(BL_ERR_DIMENSION, "Optimizer: fused dim " + std::to_string(o->d) +
+                                   " does not match the cluster dim " + std::to_string(cl->dim));
+      }
+      o->tiles = tstart[n_layers];
+      std::vector<int> tl(static_cast<size_t>(o->tiles));
+      for (int l = 0; l < n_layers; ++l)
+        for (int t = tstart[l]; t < tstart[l + 1]; ++t) tl[t] = l;
+      const size_t L = static_cast<size_t>(n_layers);
+      o->off_dev = reinterpret_cast<uint64_t*>(dalloc<double>(L + 1));
+      o->tile_layer = reinterpret_cast<int*>(dalloc<float>(tl.size()));
+      o->layer_tile_start = reinterpret_cast<int*>(dalloc<float>(L + 1));
+      cuda_check(cudaMemcpy(o->off_dev, o->off.data(), (L + 1) * 8, cudaMemcpyHostToDevice), "off");
+      cuda_check(cudaMemcpy(o->tile_layer, tl.data(), tl.size() * 4, cudaMemcpyHostToDevice), "tiles");
+      cuda_check(cudaMemcpy(o->layer_tile_start, tstart.data(), (L + 1) * 4, cudaMemcpyHostToDevice),
+                 "tile start");
+      const size_t dn = o->d + kSlack;
+      o->x = dalloc<float>(dn);
+      o->m = dalloc<float>(dn);
+      o->v = dalloc<float>(dn);
+      o->vf = dalloc<float>(dn);
+      o->c_avg = dalloc<double>(L);
+      o->r_prev = dalloc<double>(L);
+      o->coeff = dalloc<double>(L);
+      o->mag = dalloc<double>(L);
+      o->A = dalloc<float>(L);
+      o->B = dalloc<float>(L);
+      o->invc = dalloc<float>(L);
+      o->coef_x = dalloc<float>(L);
+      o->trace = dalloc<double>(4 * L);
+      o->cmean = dalloc<double>(2);
+      o->es = dalloc<float>(1);
+      o->counter = reinterpret_cast<unsigned int*>(dalloc<float>(1));
+      o->tile_sums = dalloc<double>(4 * static_cast<size_t>(o->tiles));
+      o->tile_max = dalloc<float>(static_cast<size_t>(o->tiles));
+      std::vector<double> ones(L, 1.0);
+      std::vector<float> onesf(L, 1.0f);
+      cuda_check(cudaMemcpy(o->r_prev, ones.data(), L * 8, cudaMemcpyHostToDevice), "r_prev");
+      cuda_check(cudaMemcpy(o->coeff, ones.data(), L * 8, cudaMemcpyHostToDevice), "coeff");
+      cuda_check(cudaMemcpy(o->invc, onesf.data(), L * 4, cudaMemcpyHostToDevice), "invc");
+      cuda_check(cudaMemcpy(o->cmean, ones.data(), 2 * 8, cudaMemcpyHostToDevice), "cmean");
+      cuda_check(cudaMemcpy(o->es, onesf.data(), 4, cudaMemcpyHostToDevice), "es");
+    } catch (...) {
+      bl_optimizer_destroy(o);
+      throw;
+    }
+    *out = o;
+  });
+}
+
+void bl_optimizer_destroy(bl_optimizer* o) {
+  if (!o) return;
+  DeviceGuard g(o->cl->device);
+  cudaStreamSynchronize(o->cl->stream);
+  void* bufs[] = {o->off_dev, o->tile_layer, o->layer_tile_start, o->x, o->m, o->v, o->vf,
+                  o->mprev, o->c_avg, o->r_prev, o->coeff, o->mag, o->A, o->B, o->invc, o->coef_x,
+                  o->trace, o->cmean, o->es, o->counter, o->tile_sums, o->tile_max};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  delete o;
+}
+
+bl_status bl_optimizer_step(bl_optimizer* o, bl_cluster* c, const float* const* grads,
+                            int32_t n_grads, uint64_t t, double lr, int32_t memory,
+                            bl_step_trace* trace) {
+  return guarded([&] {
+    if (c != o->cl) fail(BL_ERR_LOGIC, "step: optimizer is bound to a different cluster");
+    DeviceGuard g(c->device);
+    o->step(grads, n_grads, t, lr, memory, trace);
+  });
+}
+
+float* bl_optimizer_grad_buffer(bl_optimizer* o, int32_t worker) {
+  return bl_cluster_input_buffer(o ? o->cl : nullptr, worker);
+}
+
+bl_status bl_optimizer_get_state(bl_optimizer* o, int32_t which, float* host_out) {
+  return guarded([&] {
+    DeviceGuard g(o->cl->device);
+    o->cl->sync_and_check(&o->off);
+    const float* src = nullptr;
+    switch (which) {
+      case BL_STATE_X: src = o->x; break;
+      case BL_STATE_V: src = o->v; break;
+      case BL_STATE_V_FROZEN:
+        if (!o->has_vf) {
+          std::memset(host_out, 0, o->d * sizeof(float));
+          return;
+        }
+        src = o->vf;
+        break;
+      case BL_STATE_M:
+      case BL_STATE_M_PREV:
+        if (which == BL_STATE_M_PREV && !o->has_mprev) {
+          std::memset(host_out, 0, o->d * sizeof(float));
+          return;
+        }
+        if (which == BL_STATE_M_PREV && o->mprev_separate) {
+          src = o->mprev;
+        } else if (o->m_valid) {
+          src = o->m;
+        } else {
+          o->materialize_m(o->cl->out);
+          src = o->cl->out;
+        }
+        break;
+      default: fail(BL_ERR_INVALID_ARGUMENT, "unknown state buffer");
+    }
+    cuda_check(cudaMemcpyAsync(host_out, src, o->d * sizeof(float), cudaMemcpyDeviceToHost,
+                               o->cl->stream),
+               "state copy");
+    cuda_check(cudaStreamSynchronize(o->cl->stream), "sync");
+  });
+}
+
+bl_status bl_optimizer_set_state(bl_optimizer* o, int32_t which, const float* host_in) {
+  return guarded([&] {
+    DeviceGuard g(o->cl->device);
+    o->cl->sync_and_check(&o->off);
+    float* dst = nullptr;
+    switch (which) {
+      case BL_STATE_X: dst = o->x; break;
+      case BL_STATE_V: dst = o->v; break;
+      case BL_STATE_V_FROZEN:
+        dst = o->vf;
+        o->has_vf = true;
+        break;
+      case BL_STATE_M:
+        if (!o->m_valid && o->has_mprev && !o->mprev_separate) {
+          // m_prev keeps the value m had: materialise it before m changes.
+          if (!o->mprev) o->mprev = dalloc<float>(o->d + kSlack);
+          o->materialize_m(o->mprev);
+          o->mprev_separate = true;
+        }
+        dst = o->m;
+        o->m_valid = true;
+        break;
+      case BL_STATE_M_PREV:
+        if (!o->mprev) o->mprev = dalloc<float>(o->d + kSlack);
+        dst = o->mprev;
+        o->mprev_separate = true;
+        o->has_mprev = true;
+        if (!o->m_valid) {
+          o->materialize_m(o->m);
+          o->m_valid = true;
+        }
+        break;
+      default: fail(BL_ERR_INVALID_ARGUMENT, "unknown state buffer");
+    }
+    cuda_check(cudaMemcpyAsync(dst, host_in, o->d * sizeof(float), cudaMemcpyHostToDevice,
+                               o->cl->stream),
+               "state copy");
+    cuda_check(cudaStreamSynchronize(o->cl->stream), "sync");
+  });
+}
+
+bl_status bl_optimizer_get_scalars(bl_optimizer* o, double* c_avg, double* r_prev, double* coeff) {
+  return guarded([&] {
+    DeviceGuard g(o->cl->device);
+    o->cl->sync_and_check(&o->off);
+    const size_t L = static_cast<size_t>(o->L);
+    if (c_avg) cuda_check(cudaMemcpy(c_avg, o->c_avg, L * 8, cudaMemcpyDeviceToHost), "c_avg");
+    if (r_prev) cuda_check(cudaMemcpy(r_prev, o->r_prev, L * 8, cudaMemcpyDeviceToHost), "r_prev");
+    if (coeff) cuda_check(cudaMemcpy(coeff, o->coeff, L * 8, cudaMemcpyDeviceToHost), "coeff");
+  });
+}
+
+bl_status bl_optimizer_set_scalars(bl_optimizer* o, const double* c_avg, const double* r_prev) {
+  return guarded([&] {
+    DeviceGuard g(o->cl->device);
+    o->cl->sync_and_check(&o->off);
+    const size_t L = static_cast<size_t>(o->L);
+    if (c_avg) cuda_check(cudaMemcpy(o->c_avg, c_avg, L * 8, cudaMemcpyHostToDevice), "c_avg");
+    if (r_prev) cuda_check(cudaMemcpy(o->r_prev, r_prev, L * 8, cudaMemcpyHostToDevice), "r_prev");
+  });
+}
+
+int32_t bl_optimizer_frozen(const bl_optimizer* o) { return o && o->frozen ? 1 : 0; }
+uint64_t bl_optimizer_fused_dim(const bl_optimizer* o) { return o ? o->d : 0; }
+int32_t bl_optimizer_layer_count(const bl_optimizer* o) { return o ? o->L : 0; }
+
+}  // extern "C"

@@ -1,0 +1,155 @@
+// bl_runtime.h — host-side objects behind the C-ABI (include/bitlamb_b200.h).
+//
+// bl_cluster mirrors bitlamb::SimCluster (comm_sim.hpp:72-148): it owns the
+// worker/server residuals and the packet buffers in HBM and runs the
+// compressed / lossless collectives either over n simulated ranks in one
+// GPU's HBM (BL_MODE_SIM) or as rank r of an NCCL communicator
+// (BL_MODE_NCCL).  bl_optimizer mirrors bitlamb::Optimizer
+// (optimizers.hpp:93-145): flat fp32 x, m, v, vf with a per-layer offset table
+// and per-layer fp64 scalars, driving the cluster's kernels in one stream.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/bitlamb_b200.h"
+#include "bl_kernels.cuh"
+
+namespace bl {
+
+struct Error {
+  bl_status status;
+  std::string msg;
+};
+
+[[noreturn]] void fail(bl_status st, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+void nccl_check(ncclResult_t r, const char* what);
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+
+ private:
+  int prev_ = -1;
+  int dev_;
+};
+
+// Kernel classes for launch counting and optional CUDA-event timing.
+enum KClass : int {
+  KC_K1 = 0, KC_FIN, KC_K3, KC_K5, KC_EPI, KC_K6, KC_W1, KC_WEPI, KC_W2, KC_AVG,
+  KC_DEC, KC_MAT, KC_STATS, KC_A2A, KC_AG, KC_H2D, KC_D2H, KC_COUNT
+};
+extern const char* const kClassNames[KC_COUNT];
+
+template <typename T>
+T* dalloc(size_t n);  // zero-initialised device allocation
+
+}  // namespace bl
+
+struct bl_cluster {
+  bl_cluster_config cfg{};
+  int n = 1, rank = 0, mode = BL_MODE_SIM, device = 0, nw = 1, ns = 1, sms = 148;
+  uint64_t dim = 0, P = 0, c = 0, c_pad = 0, W = 0, slot = 0, in_stride = 0;
+  int tpc = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+
+  float* in = nullptr;          // [nw][in_stride] inputs / gradients
+  float* werr = nullptr;        // [nw][n][c_pad] raw worker residual
+  uint32_t* wpk[2] = {nullptr, nullptr};  // [nw][n][slot] worker packets (ping-pong)
+  uint32_t* rpk = nullptr;      // [n][slot] received packets (NCCL mode)
+  float* serr = nullptr;        // [ns][c_pad] raw server residual
+  uint32_t* res[2] = {nullptr, nullptr};  // [n][slot] server packets (ping-pong)
+  double* wpart = nullptr;      // [nw][n][tpc]
+  double* spart = nullptr;      // [ns][tpc]
+  float* wcmax = nullptr;       // [nw][n][tpc] (endpoint stats)
+  float* scmax = nullptr;       // [ns][tpc]
+  float* out = nullptr;         // [P + slack] decompressed result / lossless output
+  float* lrecv = nullptr;       // [n][c_pad] lossless receive buffer (NCCL mode)
+  unsigned long long* err = nullptr;  // [kErrSlots]
+  double* stat_part = nullptr;  // stats scratch
+  float* stat_max = nullptr;
+  double* stat_out = nullptr;   // [2]
+  int stat_tiles = 0;
+
+  uint64_t calls = 0;           // compressed collectives run (ping-pong index)
+  bool last_identity = false;
+  bl_volume_ledger ledger{};
+  std::vector<bl_endpoint_stats> stats;  // 2n (local endpoints refreshed)
+  uint64_t launches = 0;
+  bool profiling = false;
+  struct Ev {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Ev> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[bl::KC_COUNT] = {};
+  uint64_t prof_n[bl::KC_COUNT] = {};
+  uint64_t pending_step = 0;    // step index of the last asynchronous optimizer step
+  bool pending_is_step = false;
+
+  int cur() const { return static_cast<int>(calls & 1u); }
+  int prev() const { return static_cast<int>((calls + 1u) & 1u); }
+
+  // Event-bracketed launch bookkeeping.
+  void begin(int cls, cudaEvent_t* a);
+  void end(int cls, cudaEvent_t a, int kernels);
+  cudaEvent_t get_event();
+
+  int grid(long long tiles) const;
+  void copy_inputs(const float* const* inputs, int n_inputs, uint64_t len, int memory);
+  // One compressed collective over the inputs already in `in` (mode 0) or a
+  // stream built by the optimizer (K1 params supplied by the caller).
+  void compressed(const bl::K1Params* k1_override, int k1_mode, float es_host,
+                  const float* es_dev);
+  void lossless(bool check_finite);  // in -> out (averaged), ledger
+  void refresh_stats();
+  void check_errors(const std::vector<uint64_t>* layer_off);
+  void sync_and_check(const std::vector<uint64_t>* layer_off);
+  void ledger_compressed();
+  void ledger_lossless();
+  uint64_t chunk_payload_bits(uint64_t j) const;
+};
+
+struct bl_optimizer {
+  int variant = BL_ONEBIT_LAMB, L = 0;
+  bl_hparams hp{};
+  uint64_t d = 0;
+  bl_cluster* cl = nullptr;
+  std::vector<uint64_t> off;  // host copy of the layer table
+  uint64_t* off_dev = nullptr;
+  int* tile_layer = nullptr;
+  int* layer_tile_start = nullptr;
+  int tiles = 0;
+  float *x = nullptr, *m = nullptr, *v = nullptr, *vf = nullptr, *mprev = nullptr;
+  double *c_avg = nullptr, *r_prev = nullptr, *coeff = nullptr, *mag = nullptr;
+  float *A = nullptr, *B = nullptr, *invc = nullptr, *coef_x = nullptr;
+  double* trace = nullptr;    // [4L]
+  double* cmean = nullptr;    // [2]
+  float* es = nullptr;        // [1]
+  unsigned int* counter = nullptr;
+  double* tile_sums = nullptr;  // [tiles][4]
+  float* tile_max = nullptr;    // [tiles]
+  bool frozen = false, has_vf = false, has_mprev = false;
+  bool m_valid = true;          // m buffer holds m (else: decompressed result * invc)
+  bool mprev_separate = false;  // m_prev poked by the caller
+  uint64_t my_calls = 0;        // cluster->calls after our last compressed step
+
+  bl::LayerTiles lt() const { return {L, tiles, off_dev, tile_layer, layer_tile_start}; }
+  bool two_stage() const {
+    return variant == BL_ONEBIT_LAMB || variant == BL_LAMB_BASIC_ONEBIT || variant == BL_ONEBIT_ADAM;
+  }
+  void step(const float* const* grads, int n_grads, uint64_t t, double lr, int memory,
+            bl_step_trace* trace_out);
+  void warmup_step(uint64_t t, double lr, bool track, bool finalize, bool adam);
+  void compressed_step(double lr);
+  void materialize_m(float* dst);
+};
