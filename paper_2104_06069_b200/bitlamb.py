@@ -270,8 +270,12 @@ def _pointers(inputs, length: int):
             a = np.ascontiguousarray(np.asarray(t), dtype=np.float32)
             keep.append(a)
             ptrs[i] = a.ctypes.data
+    lens = {int(t.shape[-1]) for t in keep}
+    if len(lens) > 1:  # comm_sim.cpp:124-126 checks every input's length
+        bad = next(int(t.shape[-1]) for t in keep if int(t.shape[-1]) != length)
+        raise DimensionError(f"input length: size mismatch ({bad} vs {length})")
     return ptrs, len(items), (MEM_DEVICE if dev else MEM_HOST), keep, (
-        items[0].shape[-1] if items else length)
+        int(keep[0].shape[-1]) if keep else length)
 
 
 class SimCluster:
