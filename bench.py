@@ -54,53 +54,58 @@ def grad_sigma(sizes, seed=1):
 # clocks during the timed region (B200_PROFILING.md)
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
-              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap"]
+    """Samples SM clock and throttle reasons every ~5 ms through NVML while the
+    timed region runs (nvidia-smi's 100 ms floor is too coarse for it)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
+        self.samples: list[tuple[float, int]] = []
+        self.max_mhz = None
+
+    def _run(self):
+        import pynvml as N
+
+        while not self._stop.is_set():
+            try:
+                self.samples.append((float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)),
+                                     int(N.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __enter__(self):
+        import threading
+
+        self._stop = threading.Event()
+        self._t = None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml as N
+
+            N.nvmlInit()
+            self.h = N.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+            time.sleep(0.02)
         except Exception:
-            self.proc = None
+            self._t = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc:
-            time.sleep(0.25)
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except Exception:
-                self.proc.kill()
-                out = ""
-            self.lines = [l for l in out.splitlines() if l.strip()]
+        if self._t:
+            self._stop.set()
+            self._t.join()
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in getattr(self, "lines", []):
-            p = [x.strip() for x in line.split(",")]
-            if len(p) < 7:
-                continue
-            try:
-                sm.append(float(p[0]))
-                mx = float(p[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        sm = [c for c, _ in self.samples]
+        mask = 0
+        for _, r in self.samples:
+            mask |= r
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz,
+                "samples": len(sm), "reasons": sorted(k for k, b in self.REASONS.items() if mask & b)}
 
 
 # ---------------------------------------------------------------------------
@@ -181,7 +186,7 @@ def run_reference(args, layout, d_full: int, n: int) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="bert-large", choices=["bert-large", "bert-base", "config1"])

@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <unordered_map>
 
 #include "bl_kernels.cuh"
 
@@ -75,6 +76,54 @@ __device__ __forceinline__ void st_row4(float* row, int lane, int s, const float
   if (nvalid > 1) p[1] = v.y;
   if (nvalid > 2) p[2] = v.z;
   if (nvalid > 3) p[3] = v.w;
+}
+
+// 128-bit streaming loads with a 256-byte L2 prefetch per miss (more bytes in
+// flight per request).  _ro: read-only for the kernel's lifetime (.nc path);
+// _rw: element later overwritten by the same thread.
+__device__ __forceinline__ float4 ldg_ro(const float* p) {
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ldg_rw(const float* p) {
+  float4 v;
+  asm("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+
+// R consecutive rows (row0 + k*128, k < R) of 4 elements per lane, row0 may be
+// misaligned by s floats.  All R rows' loads issue before any rotation.
+template <int R, bool RO>
+__device__ __forceinline__ void load_rows(float4 (&out)[R], const float* row0, int lane, int s) {
+  const float* a = row0 - s + 4 * lane;
+  float4 hi[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    out[k] = RO ? ldg_ro(a + k * kRowElems) : ldg_rw(a + k * kRowElems);
+    if (s != 0 && lane == 31) hi[k] = RO ? ldg_ro(a + k * kRowElems + 4) : ldg_rw(a + k * kRowElems + 4);
+  }
+  if (s != 0) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const float4 lo = out[k];
+      float hx = __shfl_down_sync(FULL, lo.x, 1);
+      float hy = __shfl_down_sync(FULL, lo.y, 1);
+      float hz = __shfl_down_sync(FULL, lo.z, 1);
+      if (lane == 31) {
+        hx = hi[k].x;
+        hy = hi[k].y;
+        hz = hi[k].z;
+      }
+      out[k] = s == 1 ? make_float4(lo.y, lo.z, lo.w, hx)
+             : s == 2 ? make_float4(lo.z, lo.w, hx, hy)
+                      : make_float4(lo.w, hx, hy, hz);
+    }
+  }
 }
 
 __device__ __forceinline__ double warp_bfly_sum(double v) {
@@ -203,8 +252,88 @@ __global__ void __launch_bounds__(kBlock) k1_worker_compress(const K1Params p) {
       neg_m = S2 == 0.0f ? 0.0f : -S2;
       rp = rs + (i0 >> 5);
     }
-    int l = 0;
     float A = 0.f, B = 0.f, IC = 0.f;
+
+    // Fast path: the whole tile lies inside the chunk, inside the real
+    // (unpadded) data and inside one layer.  Rows are processed 4 at a time
+    // with all loads issued first; same per-element arithmetic and the same
+    // accumulation order as the general path below.
+    bool fast = MODE != 1 && i0 + kTile <= p.c && kc + i0 + kTile <= p.d;
+    if (fast && MODE == 2) {
+      const int l0 = find_layer(p.off, p.L, kc + i0);
+      fast = l0 < p.L && kc + i0 + (kTile - 1) < __ldg(p.off + l0 + 1);
+      if (fast) {
+        A = __ldg(p.A + l0);
+        B = __ldg(p.B + l0);
+        IC = __ldg(p.invc + l0);
+      }
+    }
+    if (fast) {
+      constexpr int R = 4;
+      const uint32_t sh = 4 * (lane & 7);
+      const int wsub = lane >> 3;
+      const bool stats = p.cmax != nullptr;
+      double acc = 0.0;
+      float cm = 0.0f;
+      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        float4 g[R], raw[R];
+        uint32_t wn[R], rn[R];
+        load_rows<R, true>(g, gin + r0 * kRowElems, lane, s);
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          raw[k] = ldg_rw(we + (r0 + k) * kRowElems + 4 * lane);
+          wn[k] = __ldg(pkp + 4 * (r0 + k) + wsub) >> sh;
+          rn[k] = MODE == 2 ? __ldg(rp + 4 * (r0 + k) + wsub) >> sh : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          if (MODE == 2 && !(isfinite(g[k].x) && isfinite(g[k].y) && isfinite(g[k].z) &&
+                             isfinite(g[k].w))) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (!isfinite(comp(g[k], q))) {
+                flag(p.err, kErrGrad,
+                     (static_cast<unsigned long long>(p.worker_base + w) << 40) |
+                         (kc + i0 + (r0 + k) * kRowElems + 4 * lane + q));
+              }
+            }
+          }
+          uint32_t nib = 0;
+          float4 rawn;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float v;
+            if (MODE == 0) {
+              v = comp(g[k], q);
+            } else {
+              const float mq = __fmul_rn((rn[k] >> q) & 1u ? pos_m : neg_m, IC);   // fusion.cpp:143
+              v = __fadd_rn(__fmul_rn(A, mq), __fmul_rn(B, comp(g[k], q)));     // kernels.cpp:253
+            }
+            const float rec = (wn[k] >> q) & 1u ? Sp : -Sp;
+            const float delta = __fsub_rn(comp(raw[k], q), rec);                // compression.cpp:194
+            const float corr = __fadd_rn(v, __fmul_rn(es, delta));              // :181
+            set_comp(rawn, q, __fadd_rn(v, delta));
+            nib |= static_cast<uint32_t>(corr >= 0.0f) << q;                    // :50
+            acc += fabs(static_cast<double>(corr));                              // :54
+            if (stats) {
+              const float ac = fabsf(corr);
+              cm = cm < ac ? ac : cm;
+            }
+          }
+          st4(we + (r0 + k) * kRowElems + 4 * lane, rawn);
+          store_row_bits(pkc, r0 + k, lane, nib);
+        }
+      }
+      acc = warp_bfly_sum(acc);
+      if (lane == 0) p.partials[ep * p.tpc + t] = acc;
+      if (stats) {
+        cm = warp_max(cm);
+        if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
+      }
+      continue;
+    }
+
+    int l = 0;
     int lcache = -1;
     if (MODE != 0) l = find_layer(p.off, p.L, kc + i0);
 
@@ -350,6 +479,70 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
     uint32_t* rc = p.res_cur + static_cast<size_t>(j) * p.slot + (i0 >> 5);
     const uint32_t* inw = in + (i0 >> 5);
 
+    if (NT > 0 && i0 + kTile <= p.c) {
+      // Fast path: full tile, 4 rows per batch with every load issued first.
+      constexpr int R = 4;
+      const uint32_t sh = 4 * (lane & 7);
+      const int wsub = lane >> 3;
+      const bool stats = p.cmax != nullptr;
+      double acc = 0.0;
+      float cm = 0.0f;
+      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        float4 raw[R];
+        uint32_t sn[R], wn[R][NT > 0 ? NT : 1];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          raw[k] = ldg_rw(se + (r0 + k) * kRowElems + 4 * lane);
+          sn[k] = __ldg(rs + 4 * (r0 + k) + wsub) >> sh;
+#pragma unroll
+          for (int i = 0; i < (NT > 0 ? NT : 1); ++i)
+            wn[k][i] = __ldg(inw + i * p.in_i + 4 * (r0 + k) + wsub) >> sh;
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+          for (int i = 0; i < (NT > 0 ? NT : 1); ++i) {  // compression.cpp:83-89
+            const float S = s_scale[wib][i];
+            if (S != 0.0f) {
+              const double Sd = S;
+              a0 += (wn[k][i] & 1u) ? Sd : -Sd;
+              a1 += (wn[k][i] & 2u) ? Sd : -Sd;
+              a2 += (wn[k][i] & 4u) ? Sd : -Sd;
+              a3 += (wn[k][i] & 8u) ? Sd : -Sd;
+            }
+          }
+          const float4 avg = make_float4(static_cast<float>(a0 * inv_n), static_cast<float>(a1 * inv_n),
+                                         static_cast<float>(a2 * inv_n), static_cast<float>(a3 * inv_n));
+          uint32_t nib = 0;
+          float4 rawn;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float v = comp(avg, q);
+            const float rec = (sn[k] >> q) & 1u ? S2p : -S2p;
+            const float delta = __fsub_rn(comp(raw[k], q), rec);
+            const float corr = __fadd_rn(v, __fmul_rn(es, delta));
+            set_comp(rawn, q, __fadd_rn(v, delta));
+            nib |= static_cast<uint32_t>(corr >= 0.0f) << q;
+            acc += fabs(static_cast<double>(corr));
+            if (stats) {
+              const float ac = fabsf(corr);
+              cm = cm < ac ? ac : cm;
+            }
+          }
+          st4(se + (r0 + k) * kRowElems + 4 * lane, rawn);
+          store_row_bits(rc, r0 + k, lane, nib);
+        }
+      }
+      acc = warp_bfly_sum(acc);
+      if (lane == 0) p.partials[static_cast<size_t>(sv) * p.tpc + t] = acc;
+      if (stats) {
+        cm = warp_max(cm);
+        if (lane == 0) p.cmax[static_cast<size_t>(sv) * p.tpc + t] = cm;
+      }
+      continue;
+    }
+
     double acc = 0.0;
     float cm = 0.0f;
     for (int r = 0; r < kRowsPerTile; ++r) {
@@ -452,6 +645,13 @@ __device__ __forceinline__ float4 row_mg(const BitCursor& bc, uint64_t kr, int l
   return out;
 }
 
+// Fast-path bits: the lane's 4 chunk-relative positions i..i+3 (i may sit
+// anywhere inside a word) of one packet.
+__device__ __forceinline__ uint32_t nibble_at(const uint32_t* sl, uint32_t i) {
+  const uint32_t w0 = __ldg(sl + (i >> 5)), w1 = __ldg(sl + (i >> 5) + 1);
+  return __funnelshift_r(w0, w1, i & 31u) & 0xFu;
+}
+
 __device__ __forceinline__ int lane_valid(uint64_t len, uint64_t ir, int lane) {
   const uint64_t st = ir + 4 * lane;
   if (st >= len) return 0;
@@ -484,6 +684,65 @@ __global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
     const float ic = __ldg(p.invc + l);
     uint64_t j = base / p.c, ce = (j + 1) * p.c;
     uint64_t jp = j, cep = ce;
+
+    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce) {
+      // Fast path: aligned, full tile, one chunk of the result.
+      constexpr int R = 4;
+      const uint32_t* sl = cur.res + j * p.slot;
+      const float S = slot_scale(sl, p.W);
+      const float pos = S, neg = S == 0.0f ? 0.0f : -S;
+      const uint32_t* slp = MPREV ? prv.res + j * p.slot : nullptr;
+      float posp = 0.f, negp = 0.f;
+      if (MPREV) {
+        const float Sq = slot_scale(slp, p.W);
+        posp = Sq;
+        negp = Sq == 0.0f ? 0.0f : -Sq;
+      }
+      const uint32_t ib = static_cast<uint32_t>(base - j * p.c) + 4 * lane;
+      double acc = 0.0;
+      float mx = 0.0f;
+      bool bad = false;
+      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        float4 v[R], vf[R], mpb[R];
+        uint32_t nc[R], np[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const float* row = p.v + base + (r0 + k) * kRowElems + 4 * lane;
+          v[k] = ldg_rw(row);
+          vf[k] = ldg_ro(p.vf + base + (r0 + k) * kRowElems + 4 * lane);
+          nc[k] = nibble_at(sl, ib + (r0 + k) * kRowElems);
+          if (MPREV) np[k] = nibble_at(slp, ib + (r0 + k) * kRowElems);
+          else mpb[k] = ldg_ro(p.m + base + (r0 + k) * kRowElems + 4 * lane);
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          float4 vn;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float mg = __fmul_rn((nc[k] >> q) & 1u ? pos : neg, ic);
+            const float mp = MPREV ? __fmul_rn((np[k] >> q) & 1u ? posp : negp, ic) : comp(mpb[k], q);
+            const float rec = __fadd_rn(__fmul_rn(p.inv, mg), __fmul_rn(p.ninvb, mp));
+            const float nvv = __fadd_rn(__fmul_rn(p.b2, comp(v[k], q)),
+                                        __fmul_rn(__fmul_rn(p.omb2, rec), rec));
+            set_comp(vn, q, nvv);
+            bad |= !isfinite(rec);
+            const float den = nvv < p.floor_ ? p.floor_ : nvv;
+            const float ratio = fabsf(comp(vf[k], q)) / den;
+            mx = mx < ratio ? ratio : mx;
+            acc += static_cast<double>(nvv) * static_cast<double>(nvv);
+          }
+          st4(p.v + base + (r0 + k) * kRowElems + 4 * lane, vn);
+        }
+      }
+      if (bad) flag(p.err, kErrRecon, static_cast<unsigned long long>(l));
+      acc = warp_bfly_sum(acc);
+      mx = warp_max(mx);
+      if (lane == 0) {
+        p.tile_v2[tile] = acc;
+        p.tile_max[tile] = mx;
+      }
+      continue;
+    }
 
     double acc = 0.0;
     float mx = 0.0f;
@@ -597,6 +856,36 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
     const float ic = __ldg(p.invc + l);
     const float a = __ldg(p.coef_x + l);
     uint64_t j = base / p.c, ce = (j + 1) * p.c;
+    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce) {
+      constexpr int R = 4;
+      const uint32_t* sl = cur.res + j * p.slot;
+      const float S = slot_scale(sl, p.W);
+      const float pos = S, neg = S == 0.0f ? 0.0f : -S;
+      const uint32_t ib = static_cast<uint32_t>(base - j * p.c) + 4 * lane;
+      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        float4 x[R], vf[R];
+        uint32_t nc[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          x[k] = ldg_rw(p.x + base + (r0 + k) * kRowElems + 4 * lane);
+          vf[k] = ldg_ro(p.vf + base + (r0 + k) * kRowElems + 4 * lane);
+          nc[k] = nibble_at(sl, ib + (r0 + k) * kRowElems);
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          float4 xn;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float mg = __fmul_rn((nc[k] >> q) & 1u ? pos : neg, ic);
+            float u = __fdiv_rn(mg, __fadd_rn(__fsqrt_rn(comp(vf[k], q)), p.eta));
+            if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
+            set_comp(xn, q, __fadd_rn(comp(x[k], q), __fmul_rn(a, u)));
+          }
+          st4(p.x + base + (r0 + k) * kRowElems + 4 * lane, xn);
+        }
+      }
+      continue;
+    }
     for (int r = 0; r < kRowsPerTile; ++r) {
       const uint64_t ir = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r) * kRowElems;
       if (ir >= len) break;
@@ -902,6 +1191,22 @@ __global__ void __launch_bounds__(1024) k_error_stats_final(const double* part, 
 
 __global__ void k_set_float(float* p, float v) { *p = v; }
 
+// Cap a persistent grid at the number of co-resident blocks of `kernel`.
+template <typename K>
+int resident(K kernel, int want) {
+  static thread_local std::unordered_map<const void*, int> cache;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBlock, 0);
+    it = cache.emplace(key, sms * (occ > 0 ? occ : 1)).first;
+  }
+  return want < it->second ? want : it->second;
+}
+
 int grid_for_elems(uint64_t n) {
   const uint64_t g = (n + 255) / 256;
   return static_cast<int>(g < 148 * 16 ? (g == 0 ? 1 : g) : 148 * 16);
@@ -911,9 +1216,9 @@ int grid_for_elems(uint64_t n) {
 
 int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
   switch (mode) {
-    case 0: k1_worker_compress<0><<<grid, kBlock, 0, s>>>(p); break;
-    case 1: k1_worker_compress<1><<<grid, kBlock, 0, s>>>(p); break;
-    default: k1_worker_compress<2><<<grid, kBlock, 0, s>>>(p); break;
+    case 0: k1_worker_compress<0><<<resident(k1_worker_compress<0>, grid), kBlock, 0, s>>>(p); break;
+    case 1: k1_worker_compress<1><<<resident(k1_worker_compress<1>, grid), kBlock, 0, s>>>(p); break;
+    default: k1_worker_compress<2><<<resident(k1_worker_compress<2>, grid), kBlock, 0, s>>>(p); break;
   }
   return 1;
 }
@@ -925,18 +1230,18 @@ int launch_finalize(const FinalizeParams& p, int count, cudaStream_t s) {
 
 int launch_k3(const K3Params& p, int grid, cudaStream_t s) {
   switch (p.n) {
-    case 1: k3_server_reduce<1><<<grid, kBlock, 0, s>>>(p); break;
-    case 2: k3_server_reduce<2><<<grid, kBlock, 0, s>>>(p); break;
-    case 4: k3_server_reduce<4><<<grid, kBlock, 0, s>>>(p); break;
-    case 8: k3_server_reduce<8><<<grid, kBlock, 0, s>>>(p); break;
-    default: k3_server_reduce<0><<<grid, kBlock, 0, s>>>(p); break;
+    case 1: k3_server_reduce<1><<<resident(k3_server_reduce<1>, grid), kBlock, 0, s>>>(p); break;
+    case 2: k3_server_reduce<2><<<resident(k3_server_reduce<2>, grid), kBlock, 0, s>>>(p); break;
+    case 4: k3_server_reduce<4><<<resident(k3_server_reduce<4>, grid), kBlock, 0, s>>>(p); break;
+    case 8: k3_server_reduce<8><<<resident(k3_server_reduce<8>, grid), kBlock, 0, s>>>(p); break;
+    default: k3_server_reduce<0><<<resident(k3_server_reduce<0>, grid), kBlock, 0, s>>>(p); break;
   }
   return 1;
 }
 
 int launch_k5(const K5Params& p, int grid, cudaStream_t s) {
-  if (p.res_prev) k5_update_a<1><<<grid, kBlock, 0, s>>>(p);
-  else k5_update_a<0><<<grid, kBlock, 0, s>>>(p);
+  if (p.res_prev) k5_update_a<1><<<resident(k5_update_a<1>, grid), kBlock, 0, s>>>(p);
+  else k5_update_a<0><<<resident(k5_update_a<0>, grid), kBlock, 0, s>>>(p);
   return 1;
 }
 
@@ -946,12 +1251,12 @@ int launch_epilogue(const EpiParams& p, cudaStream_t s) {
 }
 
 int launch_k6(const K6Params& p, int grid, cudaStream_t s) {
-  k6_update_b<<<grid, kBlock, 0, s>>>(p);
+  k6_update_b<<<resident(k6_update_b, grid), kBlock, 0, s>>>(p);
   return 1;
 }
 
 int launch_w1(const W1Params& p, int grid, cudaStream_t s) {
-  kw1_warmup_a<<<grid, kBlock, 0, s>>>(p);
+  kw1_warmup_a<<<resident(kw1_warmup_a, grid), kBlock, 0, s>>>(p);
   return 1;
 }
 
@@ -961,7 +1266,7 @@ int launch_wepilogue(const WEpiParams& p, cudaStream_t s) {
 }
 
 int launch_w2(const W2Params& p, int grid, cudaStream_t s) {
-  kw2_warmup_b<<<grid, kBlock, 0, s>>>(p);
+  kw2_warmup_b<<<resident(kw2_warmup_b, grid), kBlock, 0, s>>>(p);
   return 1;
 }
 

@@ -100,7 +100,7 @@ void bl_cluster::end(int cls, cudaEvent_t a, int kernels) {
 
 int bl_cluster::grid(long long tiles) const {
   const long long want = (tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const long long cap = static_cast<long long>(sms) * 8;
+  const long long cap = static_cast<long long>(sms) * 16;  // launchers cap at residency
   return static_cast<int>(std::max<long long>(1, std::min(want, cap)));
 }
 
