@@ -218,8 +218,8 @@ __device__ __forceinline__ void flag(unsigned long long* err, int slot, unsigned
 // materialised from the previous packet when read.  Identical arithmetic,
 // one pass: 12 B/elem read + 4 B/elem written + 1 bit.
 // ---------------------------------------------------------------------------
-template <int MODE>
-__global__ void __launch_bounds__(kBlock) k1_worker_compress(const K1Params p) {
+template <int MODE, bool ALIGNED>
+__global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kBlock) k1_worker_compress(const K1Params p) {
     const int t = static_cast<int>(rem - static_cast<long long>(j) * p.tpc);
     const uint64_t i0 = static_cast<uint64_t>(t) * kTile;  // chunk-relative
     const uint64_t kc = static_cast<uint64_t>(j) * p.c;    // global chunk start
-    const int s = static_cast<int>(kc & 3u);
+    const int s = ALIGNED ? 0 : static_cast<int>(kc & 3u);  // ALIGNED: c % 4 == 0
     const size_t ep = static_cast<size_t>(w) * p.n + j;    // endpoint (worker, chunk)
     const float* gin = p.in + static_cast<size_t>(w) * p.in_stride + kc + i0;
     float* we = p.werr + ep * p.c_pad + i0;
@@ -1215,11 +1215,14 @@ int grid_for_elems(uint64_t n) {
 }  // namespace
 
 int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
+#define BL_K1(M, A) k1_worker_compress<M, A><<<resident(k1_worker_compress<M, A>, grid), kBlock, 0, s>>>(p)
+  const bool al = (p.c & 3u) == 0;  // every chunk start 16-byte aligned
   switch (mode) {
-    case 0: k1_worker_compress<0><<<resident(k1_worker_compress<0>, grid), kBlock, 0, s>>>(p); break;
-    case 1: k1_worker_compress<1><<<resident(k1_worker_compress<1>, grid), kBlock, 0, s>>>(p); break;
-    default: k1_worker_compress<2><<<resident(k1_worker_compress<2>, grid), kBlock, 0, s>>>(p); break;
+    case 0: if (al) BL_K1(0, true); else BL_K1(0, false); break;
+    case 1: BL_K1(1, false); break;
+    default: if (al) BL_K1(2, true); else BL_K1(2, false); break;
   }
+#undef BL_K1
   return 1;
 }
 
