@@ -1,0 +1,131 @@
+"""Multi-GPU parity check (run under torchrun, one process per GPU).
+
+Every rank runs the NCCL-mode cluster/optimizer on its own GPU with its own
+gradient; rank 0 additionally runs the same n-worker job in SIM mode on its
+GPU.  The real collective must reproduce the simulated one bit-for-bit:
+worker packets, server packets, residuals, results, and the replicated
+optimizer state after every step (warmup with the deterministic lossless
+all-reduce, freeze, compression stage).
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/multigpu_check.py
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2104_06069_b200 import bitlamb as bl  # noqa: E402
+
+
+def gather_bytes(b: bytes) -> list[bytes]:
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, b)
+    return out
+
+
+def main() -> int:
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(bl.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    uid_b = bytes(uid.cpu().numpy().tobytes())
+    failures = []
+
+    def check(cond, what):
+        if not cond:
+            failures.append(what)
+
+    # ---- 1. compressed_allreduce API: real vs sim --------------------------
+    for d in (37, 10001, 4096 * 5 + 3, 1_000_003):
+        cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=uid_b)
+        sim = bl.SimCluster(world, d, device=local) if rank == 0 else None
+        rng = np.random.default_rng(d)
+        for step in range(3):
+            x = rng.standard_normal((world, d)).astype(np.float32)
+            es = 1.0 if step < 2 else 0.6
+            out = cl.compressed_allreduce(x[rank], error_scale=es)
+            outs = gather_bytes(out.tobytes())
+            pk = gather_bytes(b"".join(cl.packet(rank, j) for j in range(world)))
+            sp = gather_bytes(cl.server_packet(rank))
+            we = gather_bytes(cl.worker_error(rank).tobytes())
+            se = gather_bytes(cl.server_error(rank).tobytes())
+            if rank == 0:
+                ref = sim.compressed_allreduce(x, error_scale=es)
+                for r in range(world):
+                    check(outs[r] == ref.tobytes(), f"d={d} step={step} result rank {r}")
+                    check(pk[r] == b"".join(sim.packet(r, j) for j in range(world)),
+                          f"d={d} step={step} worker packets rank {r}")
+                    check(sp[r] == sim.server_packet(r), f"d={d} step={step} server packet {r}")
+                    check(we[r] == sim.worker_error(r).tobytes(), f"d={d} step={step} werr {r}")
+                    check(se[r] == sim.server_error(r).tobytes(), f"d={d} step={step} serr {r}")
+        led = cl.ledger()
+        if rank == 0:
+            check(led == sim.ledger(), f"d={d} ledger")
+        lo = cl.lossless_allreduce(x[rank])
+        los = gather_bytes(lo.tobytes())
+        if rank == 0:
+            ref = sim.lossless_allreduce(x)
+            check(all(b == ref.tobytes() for b in los), f"d={d} lossless")
+        cl.close()
+        if sim:
+            sim.close()
+
+    # ---- 2. optimizer: warmup + freeze + compression stage -----------------
+    sizes = [3000, 2, 1024, 1023, 5000, 3, 4096 * 3 + 17, 77777]
+    d = sum(sizes)
+    steps, warm = 16, 5
+    hp = bl.HyperParams(total_steps=steps, warmup_steps=warm, weight_decay=0.01,
+                        scaled_error_feedback=True)
+    cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=uid_b)
+    opt = bl.Optimizer("onebit_lamb", sizes, hp, cl)
+    if rank == 0:
+        sim = bl.SimCluster(world, d, device=local)
+        sopt = bl.Optimizer("onebit_lamb", sizes, hp, sim)
+    rng = np.random.default_rng(7)
+    x0 = (rng.standard_normal(d) * 0.02).astype(np.float32)
+    opt.set("x", x0)
+    if rank == 0:
+        sopt.set("x", x0)
+    sig = np.repeat(10.0 ** (-4 + 2 * rng.random(len(sizes))), sizes).astype(np.float32)
+    for t in range(steps):
+        g = (rng.standard_normal((world, d)) * sig).astype(np.float32)
+        tr = opt.step(g[rank:rank + 1], t, 1e-3)
+        xs = gather_bytes(opt.get("x").tobytes())
+        trs = gather_bytes(tr.c.tobytes() + tr.r.tobytes() + tr.v_norm.tobytes())
+        if rank == 0:
+            st = sopt.step(g, t, 1e-3)
+            ref_x = sopt.get("x").tobytes()
+            for r in range(world):
+                check(xs[r] == ref_x, f"optimizer x rank {r} t={t}")
+                check(trs[r] == st.c.tobytes() + st.r.tobytes() + st.v_norm.tobytes(),
+                      f"optimizer trace rank {r} t={t}")
+    for k in ("m", "v", "v_frozen"):
+        vals = gather_bytes(opt.get(k).tobytes())
+        if rank == 0:
+            ref = sopt.get(k).tobytes()
+            check(all(v == ref for v in vals), f"optimizer {k}")
+
+    ok = torch.tensor([0 if failures else 1], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(("MULTIGPU PASS" if ok.item() else "MULTIGPU FAIL") + f" world={world}", flush=True)
+    if failures:
+        print(f"rank {rank} failures: {failures[:10]}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0 if ok.item() else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
