@@ -96,34 +96,37 @@ __device__ __forceinline__ float4 ldg_rw(const float* p) {
   return v;
 }
 
+__device__ __forceinline__ float2 ldg2_ro(const float* p) {
+  float2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ldg1_ro(const float* p) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+// Lane's 4 elements p[0..3] where p sits s floats past a 16-byte boundary:
+// one 128-bit load when aligned, 64+64 when s == 2, 32+64+32 when s is odd
+// (every access naturally aligned; no lane exchange).
+__device__ __forceinline__ float4 ldg_mis_ro(const float* p, int s) {
+  if (s == 0) return ldg_ro(p);
+  if (s == 2) {
+    const float2 a = ldg2_ro(p), b = ldg2_ro(p + 2);
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  const float2 m = ldg2_ro(p + 1);
+  return make_float4(ldg1_ro(p), m.x, m.y, ldg1_ro(p + 3));
+}
+
 // R consecutive rows (row0 + k*128, k < R) of 4 elements per lane, row0 may be
-// misaligned by s floats.  All R rows' loads issue before any rotation.
+// misaligned by s floats.
 template <int R, bool RO>
 __device__ __forceinline__ void load_rows(float4 (&out)[R], const float* row0, int lane, int s) {
-  const float* a = row0 - s + 4 * lane;
-  float4 hi[R];
+  const float* a = row0 + 4 * lane;
 #pragma unroll
-  for (int k = 0; k < R; ++k) {
-    out[k] = RO ? ldg_ro(a + k * kRowElems) : ldg_rw(a + k * kRowElems);
-    if (s != 0 && lane == 31) hi[k] = RO ? ldg_ro(a + k * kRowElems + 4) : ldg_rw(a + k * kRowElems + 4);
-  }
-  if (s != 0) {
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const float4 lo = out[k];
-      float hx = __shfl_down_sync(FULL, lo.x, 1);
-      float hy = __shfl_down_sync(FULL, lo.y, 1);
-      float hz = __shfl_down_sync(FULL, lo.z, 1);
-      if (lane == 31) {
-        hx = hi[k].x;
-        hy = hi[k].y;
-        hz = hi[k].z;
-      }
-      out[k] = s == 1 ? make_float4(lo.y, lo.z, lo.w, hx)
-             : s == 2 ? make_float4(lo.z, lo.w, hx, hy)
-                      : make_float4(lo.w, hx, hy, hz);
-    }
-  }
+  for (int k = 0; k < R; ++k) out[k] = RO ? ldg_mis_ro(a + k * kRowElems, s) : ldg_rw(a + k * kRowElems);
 }
 
 __device__ __forceinline__ double warp_bfly_sum(double v) {

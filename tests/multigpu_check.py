@@ -35,11 +35,14 @@ def main() -> int:
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-    if rank == 0:
-        uid.copy_(torch.frombuffer(bytearray(bl.nccl_unique_id()), dtype=torch.uint8))
-    dist.broadcast(uid, 0)
-    uid_b = bytes(uid.cpu().numpy().tobytes())
+    def new_uid() -> bytes:
+        """A fresh NCCL unique id per communicator, broadcast from rank 0."""
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(bl.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        return bytes(uid.cpu().numpy().tobytes())
+
     failures = []
 
     def check(cond, what):
@@ -48,7 +51,7 @@ def main() -> int:
 
     # ---- 1. compressed_allreduce API: real vs sim --------------------------
     for d in (37, 10001, 4096 * 5 + 3, 1_000_003):
-        cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=uid_b)
+        cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid())
         sim = bl.SimCluster(world, d, device=local) if rank == 0 else None
         rng = np.random.default_rng(d)
         for step in range(3):
@@ -87,7 +90,7 @@ def main() -> int:
     steps, warm = 16, 5
     hp = bl.HyperParams(total_steps=steps, warmup_steps=warm, weight_decay=0.01,
                         scaled_error_feedback=True)
-    cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=uid_b)
+    cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid())
     opt = bl.Optimizer("onebit_lamb", sizes, hp, cl)
     if rank == 0:
         sim = bl.SimCluster(world, d, device=local)
