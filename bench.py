@@ -311,6 +311,16 @@ def main():
     peak, peak_kind = hbm_peak()
     dom = max((k for k in kern if k in ab), key=lambda k: kern[k]["ms_per_launch"] * kern[k]["launches"])
     achieved = ab[dom] / (kern[dom]["ms_per_launch"] * 1e-3) / 1e9
+    traffic, traffic_src = None, None
+    import glob
+
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if caps and args.workload == "bert-large" and cl.n_workers() == 1:
+        with open(caps[-1]) as f:
+            tj = json.load(f)
+        if dom in tj:
+            traffic = tj[dom]["dram_bytes"]
+            traffic_src = os.path.relpath(caps[-1], ROOT)
     for k in kern:
         if k in ab:
             kern[k]["gbs"] = ab[k] / (kern[k]["ms_per_launch"] * 1e-3) / 1e9
@@ -364,7 +374,8 @@ def main():
                        "l2": "inputs larger than L2 (1.34 GB per state buffer vs 126 MB L2)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "algorithmic_bytes": ab[dom]},
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes": ab[dom]},
             "kernels": kern,
             "compressed_allreduce_ms": comm_ms,
             "compressed_allreduce_algbw_gbs": 4 * d / (comm_ms * 1e-3) / 1e9 if comm_ms else None,
