@@ -166,18 +166,21 @@ def reference_sample(layout, n: int, target_params: int = 12_000_000, steps: int
 
 
 def cpu_cores() -> int:
-    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    """Host threads given to the reference: BL_REF_THREADS, else every core
+    (torchrun exports OMP_NUM_THREADS=1, which must not throttle the baseline)."""
+    return int(os.environ.get("BL_REF_THREADS", os.cpu_count() or 1))
 
 
 def run_reference(args, layout, d_full: int, n: int) -> dict:
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
-    os.environ.setdefault("OMP_PROC_BIND", "close")
+    from oracle import oracle as O
+
+    cores = O.set_reference_threads(cpu_cores())
     s, d_s, L_s = reference_sample(layout, n, steps=max(1, min(args.steps, 3)))
     ms = s * 1e3 * d_full / d_s
     sample = (f"reference Optimizer::step (compression stage, n={n} simulated workers) on the "
               f"first {L_s} BERT-Large tensors ({d_s:,} params), median of "
               f"{max(1, min(args.steps, 3))} steps, extrapolated x{d_full / d_s:.2f} by parameter count")
-    return {"value": ms, "unit": "ms", "cores": cpu_cores(), "kind": "reference", "sample": sample}
+    return {"value": ms, "unit": "ms", "cores": cores, "kind": "reference", "sample": sample}
 
 
 # ---------------------------------------------------------------------------
@@ -354,7 +357,7 @@ def main():
     del grads
     torch.cuda.empty_cache()
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cpu = run_reference(args, layout, d, cl.n_workers())
         except Exception as exc:  # reported, never silently replaced

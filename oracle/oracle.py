@@ -114,6 +114,9 @@ class Lib:
         so.oc_opt_get_scalars.argtypes = [P, P]
         so.oc_opt_set_scalars.argtypes = [P, P]
         so.oc_opt_frozen.argtypes = [P]
+        if which == "ref":
+            so.oc_set_threads.argtypes = [C.c_int]
+            so.oc_set_threads.restype = C.c_int
         if which != "ref":
             so.oc_cluster_set_tolerance.argtypes = [P, C.c_double]
             so.oc_cluster_server_packet.argtypes = [P, C.c_int, P]
@@ -129,6 +132,11 @@ class Lib:
 
     def arr(self, a) -> np.ndarray:
         return np.ascontiguousarray(a, dtype=self.real)
+
+
+def set_reference_threads(n: int) -> int:
+    """OpenMP threads used by the reference library; returns the team size."""
+    return int(lib("ref").so.oc_set_threads(int(n)))
 
 
 def lib(which: str) -> Lib:

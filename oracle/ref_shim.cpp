@@ -25,6 +25,10 @@
 #include <string>
 #include <vector>
 
+#if defined(_OPENMP)
+#include <omp.h>
+#endif
+
 // Standard headers are included first so the macro below only opens the
 // reference's own classes.
 #define private public
@@ -112,6 +116,18 @@ extern "C" {
 
 const char* oc_last_error() { return g_err.c_str(); }
 int oc_real_bytes() { return 8; }
+
+// OpenMP team size for the reference's parallel loops (the reference itself
+// reads OMP_NUM_THREADS; launchers such as torchrun force it to 1).
+int oc_set_threads(int n) {
+#if defined(_OPENMP)
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
+}
 
 // ---- SimCluster -----------------------------------------------------------
 int oc_cluster_new(int n, std::uint64_t dim, int kind, int baseline_bits,

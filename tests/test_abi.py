@@ -149,7 +149,7 @@ def test_bench_reference_arm_prints_contract_line():
 
     if not have_ref():
         pytest.skip("oracle/_ref not built")
-    env = dict(os.environ, OMP_NUM_THREADS="4")
+    env = dict(os.environ, BL_REF_THREADS="4")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
                         "--steps", "1", "--warmup", "0", "--workload", "config1"],
                        capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
