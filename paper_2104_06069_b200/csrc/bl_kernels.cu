@@ -29,9 +29,6 @@ __device__ __forceinline__ float4 ld4_cs(const float* p) {
   return __ldcs(reinterpret_cast<const float4*>(p));
 }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
-__device__ __forceinline__ void st4_cs(float* p, float4 v) {
-  __stcs(reinterpret_cast<float4*>(p), v);
-}
 
 __device__ __forceinline__ float comp(const float4& v, int q) {
   return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
@@ -688,7 +685,8 @@ __global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
     uint64_t j = base / p.c, ce = (j + 1) * p.c;
     uint64_t jp = j, cep = ce;
 
-    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce) {
+    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce && !p.dense &&
+        !p.norm_only) {
       // Fast path: aligned, full tile, one chunk of the result.
       constexpr int R = 4;
       const uint32_t* sl = cur.res + j * p.slot;
@@ -756,11 +754,32 @@ __global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
       const uint64_t kr = base + static_cast<uint64_t>(r) * kRowElems;
       const int nv = lane_valid(len, ir, lane);
       const float4 v = ld_row4<false>(p.v + kr, lane, s);
+      if (p.norm_only) {  // optimizers.cpp:324 trace ||v|| only (v is not updated)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < nv) acc += static_cast<double>(comp(v, q)) * static_cast<double>(comp(v, q));
+        if (p.m_store) {  // identity compressor: m = m_g (:319)
+          const float4 dv = ld_row4<false>(p.dense + kr, lane, s);
+          float4 mg;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) set_comp(mg, q, __fmul_rn(comp(dv, q), ic));
+          st_row4(p.m_store + kr, lane, s, mg, nv);
+        }
+        continue;
+      }
       const float4 vf = ld_row4<false>(p.vf + kr, lane, s);
-      const float4 mg = row_mg(cur, kr, lane, ic, j, ce);
+      float4 mg;
+      if (p.dense) {
+        const float4 dv = ld_row4<false>(p.dense + kr, lane, s);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) set_comp(mg, q, __fmul_rn(comp(dv, q), ic));  // fusion.cpp:143
+      } else {
+        mg = row_mg(cur, kr, lane, ic, j, ce);
+      }
       float4 mp;
       if (MPREV == 0) mp = ld_row4<false>(p.m + kr, lane, s);
       else mp = row_mg(prv, kr, lane, ic, jp, cep);
+      if (p.m_store) st_row4(p.m_store + kr, lane, s, mg, nv);  // m = m_g (:319)
       float4 vn;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -810,16 +829,21 @@ __global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
   mx = block1024_max(mx, shf);
   if (threadIdx.x == 0) {
     const int L = p.L;
-    const double pre = static_cast<double>(mx);
-    const double rp = p.r_prev[l];
-    // vector_ops.cpp:25-28 clip = min(max(x, a), b)
-    const double lo1 = (1.0 - p.r_thr) * rp, hi1 = (1.0 + p.r_thr) * rp;
-    double r = pre < lo1 ? lo1 : pre;
-    r = hi1 < r ? hi1 : r;
-    r = r < p.r_min ? p.r_min : r;
-    r = p.r_max < r ? p.r_max : r;
-    const double c = r * p.c_avg[l];
-    p.r_prev[l] = r;
+    double pre = 1.0, r = 1.0, c = 1.0;
+    if (p.mode == 0) {
+      pre = static_cast<double>(mx);
+      const double rp = p.r_prev[l];
+      // vector_ops.cpp:25-28 clip = min(max(x, a), b)
+      const double lo1 = (1.0 - p.r_thr) * rp, hi1 = (1.0 + p.r_thr) * rp;
+      r = pre < lo1 ? lo1 : pre;
+      r = hi1 < r ? hi1 : r;
+      r = r < p.r_min ? p.r_min : r;
+      r = p.r_max < r ? p.r_max : r;
+      c = r * p.c_avg[l];
+      p.r_prev[l] = r;
+    } else if (p.mode == 1) {
+      c = p.c_avg[l];  // optimizers.cpp:301-303
+    }
     p.coef_x[l] = static_cast<float>(-p.lr * c);
     p.trace[l] = c;
     p.trace[L + l] = r;
@@ -859,7 +883,7 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
     const float ic = __ldg(p.invc + l);
     const float a = __ldg(p.coef_x + l);
     uint64_t j = base / p.c, ce = (j + 1) * p.c;
-    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce) {
+    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce && !p.dense) {
       constexpr int R = 4;
       const uint32_t* sl = cur.res + j * p.slot;
       const float S = slot_scale(sl, p.W);
@@ -896,7 +920,14 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
       const int nv = lane_valid(len, ir, lane);
       const float4 x = ld_row4<false>(p.x + kr, lane, s);
       const float4 vf = ld_row4<false>(p.vf + kr, lane, s);
-      const float4 mg = row_mg(cur, kr, lane, ic, j, ce);
+      float4 mg;
+      if (p.dense) {
+        const float4 dv = ld_row4<false>(p.dense + kr, lane, s);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) set_comp(mg, q, __fmul_rn(comp(dv, q), ic));
+      } else {
+        mg = row_mg(cur, kr, lane, ic, j, ce);
+      }
       float4 xn;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -1194,6 +1225,22 @@ __global__ void __launch_bounds__(1024) k_error_stats_final(const double* part, 
 
 __global__ void k_set_float(float* p, float v) { *p = v; }
 
+__global__ void k_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const float* m,
+                               const uint64_t* off, int L, const float* A, const float* B,
+                               unsigned long long* err, int worker_base) {
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < d;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int l = find_layer(off, L, k);
+    const float a = __ldg(A + l), b = __ldg(B + l), mk = m[k];
+    for (int w = 0; w < nw; ++w) {
+      float* g = in + static_cast<size_t>(w) * stride + k;
+      const float gv = *g;
+      if (!isfinite(gv)) flag(err, kErrGrad, (static_cast<unsigned long long>(worker_base + w) << 40) | k);
+      *g = __fadd_rn(__fmul_rn(a, mk), __fmul_rn(b, gv));  // kernels.cpp:253
+    }
+  }
+}
+
 // Cap a persistent grid at the number of co-resident blocks of `kernel`.
 template <typename K>
 int resident(K kernel, int want) {
@@ -1310,6 +1357,13 @@ int launch_error_stats(const float* raw, uint64_t c_pad, const uint32_t* pk, uin
       raw, c_pad, pk, slot, W, c, len, scratch, scratch_max, scratch_tiles);
   k_error_stats_final<<<1, 1024, 0, s>>>(scratch, scratch_max, scratch_tiles, out);
   return 2;
+}
+
+int launch_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const float* m,
+                        const uint64_t* off, int L, const float* A, const float* B,
+                        unsigned long long* err, int worker_base, cudaStream_t s) {
+  k_build_stream<<<grid_for_elems(d), 256, 0, s>>>(in, stride, nw, d, m, off, L, A, B, err, worker_base);
+  return 1;
 }
 
 int launch_set_float(float* p, float v, cudaStream_t s) {

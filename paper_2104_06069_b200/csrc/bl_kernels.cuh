@@ -109,6 +109,9 @@ struct K5Params {
   float* tile_max;           // [tiles]
   double* tile_v2;           // [tiles]
   unsigned long long* err;
+  const float* dense;        // identity compressor: dense result (m_g = dense * invc)
+  float* m_store;            // identity compressor: m <- m_g
+  int norm_only;             // lamb_basic_1bit / onebit_adam: only ||v||^2 partials
 };
 
 struct EpiParams {
@@ -125,6 +128,7 @@ struct EpiParams {
   unsigned int* counter;
   double lr, r_thr, r_min, r_max, floor_;
   int scaled_ef;
+  int mode;  // 0 onebit_lamb (ratio rule), 1 lamb_basic_1bit (c = c_avg), 2 onebit_adam (c = 1)
 };
 
 struct K6Params {
@@ -137,6 +141,7 @@ struct K6Params {
   const float* vf;
   float* x;
   float eta, wd;
+  const float* dense;  // identity compressor: dense result
 };
 
 struct W1Params {
@@ -206,5 +211,10 @@ int launch_error_stats(const float* raw, uint64_t c_pad, const uint32_t* pk, uin
                        uint64_t W, uint64_t c, uint64_t len, double* scratch, int scratch_tiles,
                        float* scratch_max, double* out, cudaStream_t s);
 int launch_set_float(float* p, float v, cudaStream_t s);
+// Identity-compressor stream build in place (optimizers.cpp:248-255):
+// in[w][k] = A_l*m[k] + B_l*in[w][k] for k < d, with the gradient finite check.
+int launch_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const float* m,
+                        const uint64_t* off, int L, const float* A, const float* B,
+                        unsigned long long* err, int worker_base, cudaStream_t s);
 
 }  // namespace bl

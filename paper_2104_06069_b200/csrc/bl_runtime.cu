@@ -422,31 +422,41 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
 }
 
 void bl_optimizer::compressed_step(double lr) {
-  if (cl->cfg.compressor != BL_COMPRESSOR_ONEBIT) {
-    fail(BL_ERR_UNSUPPORTED, "compressed step with the identity compressor is not on the B200 path");
+  const bool identity = cl->cfg.compressor != BL_COMPRESSOR_ONEBIT;
+  // optimizers.cpp:271-303: ratio rule (onebit_lamb), c = c_avg (basic), c = 1 (adam)
+  const int emode = variant == BL_ONEBIT_LAMB ? 0 : variant == BL_LAMB_BASIC_ONEBIT ? 1 : 2;
+  cudaEvent_t a;
+  if (identity) {
+    // Identity compressor (compression.cpp:184-188): the collective is the
+    // exact ascending-worker average of the streams; residuals stay zero.
+    cl->begin(KC_AVG, &a);
+    cl->end(KC_AVG, a,
+            launch_build_stream(cl->in, cl->in_stride, cl->nw, d, m_valid ? m : nullptr, off_dev, L,
+                                A, B, cl->err, cl->mode == BL_MODE_SIM ? 0 : cl->rank, cl->stream));
+    cl->lossless(false);
+    cl->ledger_compressed();
+    cl->calls += 1;
+    cl->last_identity = true;
+  } else {
+    const int mode = m_valid ? 1 : 2;
+    if (!m_valid && cl->calls != my_calls) {
+      fail(BL_ERR_LOGIC,
+           "momentum is encoded by the cluster's last result packets, but the cluster ran another "
+           "collective since the last optimizer step");
+    }
+    K1Params p{};
+    p.L = L;
+    p.m = m;
+    p.res_prev = cl->res[cl->prev()];  // latest result before this collective
+    p.off = off_dev;
+    p.A = A;
+    p.B = B;
+    p.invc = invc;
+    cl->compressed(&p, mode, 1.0f, es);
   }
-  if (variant != BL_ONEBIT_LAMB) {
-    fail(BL_ERR_UNSUPPORTED, "compression stage of this variant is not on the B200 path yet");
-  }
-  int mode = m_valid ? 1 : 2;
-  if (!m_valid && cl->calls != my_calls) {
-    fail(BL_ERR_LOGIC,
-         "momentum is encoded by the cluster's last result packets, but the cluster ran another "
-         "collective since the last optimizer step");
-  }
-  K1Params p{};
-  p.L = L;
-  p.m = m;
-  p.res_prev = cl->res[cl->prev()];  // latest result before this collective
-  p.off = off_dev;
-  p.A = A;
-  p.B = B;
-  p.invc = invc;
-  cl->compressed(&p, mode, 1.0f, es);
 
   const int latest = static_cast<int>((cl->calls + 1u) & 1u);
   const int before = static_cast<int>(cl->calls & 1u);
-  cudaEvent_t a;
   K5Params k5{};
   k5.lt = lt();
   k5.n = cl->n;
@@ -454,8 +464,11 @@ void bl_optimizer::compressed_step(double lr) {
   k5.slot = cl->slot;
   k5.W = cl->W;
   k5.res_cur = cl->res[latest];
-  const bool mprev_buf = m_valid || mprev_separate;
+  const bool mprev_buf = m_valid || mprev_separate || identity;
   k5.res_prev = mprev_buf ? nullptr : cl->res[before];
+  k5.dense = identity ? cl->out : nullptr;
+  k5.m_store = identity ? m : nullptr;
+  k5.norm_only = emode != 0;
   k5.m = mprev_separate ? mprev : m;
   k5.invc = invc;
   k5.v = v;
@@ -490,6 +503,7 @@ void bl_optimizer::compressed_step(double lr) {
   ep.r_max = hp.r_max;
   ep.floor_ = hp.division_floor;
   ep.scaled_ef = hp.scaled_error_feedback;
+  ep.mode = emode;
   cl->begin(KC_EPI, &a);
   cl->end(KC_EPI, a, launch_epilogue(ep, cl->stream));
 
@@ -506,10 +520,11 @@ void bl_optimizer::compressed_step(double lr) {
   k6.x = x;
   k6.eta = static_cast<float>(hp.eta);
   k6.wd = static_cast<float>(hp.weight_decay);
+  k6.dense = identity ? cl->out : nullptr;
   cl->begin(KC_K6, &a);
   cl->end(KC_K6, a, launch_k6(k6, cl->grid(tiles), cl->stream));
 
-  m_valid = false;
+  m_valid = identity;  // identity: m stored by K5; one-bit: m == decompressed result * invc
   mprev_separate = false;
   my_calls = cl->calls;
 }

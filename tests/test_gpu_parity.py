@@ -245,16 +245,16 @@ def test_endpoint_stats_match_oracle(bl):
 # Optimizer (optimizers.cpp:334-364): warmup LAMB, freeze, compression stage
 # ---------------------------------------------------------------------------
 def run_pair(bl, sizes, n, steps, warmup, seed, lr=1e-3, wd=0.0, scaled=False, check_every=1,
-             grad_sigma=None):
+             grad_sigma=None, variant="onebit_lamb", kind="onebit"):
     hp = bl.HyperParams(total_steps=steps, warmup_steps=warmup, weight_decay=wd,
                         scaled_error_feedback=scaled)
     ohp = O.HyperParams(total_steps=steps, warmup_steps=warmup, weight_decay=wd,
                         scaled_error_feedback=scaled)
     d = sum(sizes)
-    cl = bl.SimCluster(n, d)
-    opt = bl.Optimizer("onebit_lamb", sizes, hp, cl)
-    ocl = O.Cluster("f32", n, d)
-    oopt = O.Optimizer("f32", "onebit_lamb", sizes, ohp)
+    cl = bl.SimCluster(n, d, compressor=kind)
+    opt = bl.Optimizer(variant, sizes, hp, cl)
+    ocl = O.Cluster("f32", n, d, kind=kind)
+    oopt = O.Optimizer("f32", variant, sizes, ohp)
     rng = np.random.default_rng(seed)
     x0 = (rng.standard_normal(d) * 0.02).astype(np.float32)
     opt.set("x", x0)
@@ -285,6 +285,20 @@ def test_optimizer_onebit_lamb_bitexact_vs_oracle_f32(bl, n):
     for i in range(n):
         assert_same(cl.worker_error(i), ocl.worker_error(i))
         assert_same(cl.server_error(i), ocl.server_error(i))
+
+
+@pytest.mark.parametrize("variant", ["lamb_basic_1bit", "onebit_adam", "lamb", "adam"])
+def test_optimizer_other_variants_bitexact(bl, variant):
+    """The reference's ablation/baseline variants (optimizers.cpp:140-200,
+    301-303) through the same kernels."""
+    run_pair(bl, [3000, 2, 1024, 4099], 2, steps=14, warmup=5, seed=21, variant=variant)
+
+
+@pytest.mark.parametrize("variant", ["onebit_lamb", "lamb_basic_1bit"])
+def test_optimizer_identity_compressor_bitexact(bl, variant):
+    """Identity compressor inside the optimizer (the reference's lossless-collapse
+    setup, test_optimizers.cpp:381-438)."""
+    run_pair(bl, [5, 9, 4096 + 3], 4, steps=20, warmup=6, seed=91, variant=variant, kind="identity")
 
 
 def test_optimizer_weight_decay_and_scaled_feedback(bl):
