@@ -197,6 +197,8 @@ def main():
                     help="simulate this many ranks on one GPU instead of one rank per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="NCCL-mode packet exchange: fused NVLink peer stores or NCCL")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
 
@@ -245,7 +247,7 @@ def main():
         dist.broadcast(uid, 0)
         cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local,
                            nccl_unique_id=bytes(uid.cpu().numpy().tobytes()),
-                           stream=stream.cuda_stream)
+                           stream=stream.cuda_stream, transport=args.transport)
     else:
         cl = bl.SimCluster(n, d, device=local, stream=stream.cuda_stream)
     nw = cl.local_workers()
@@ -373,6 +375,7 @@ def main():
             "config": {"workload": f"{args.workload} 1-bit LAMB compression-stage step",
                        "params": d, "layers": len(sizes), "world": cl.n_workers(),
                        "mode": "nccl" if world > 1 else ("sim" if n > 1 else "single"),
+                       "transport": cl.transport,
                        "parallelism": f"dp{cl.n_workers()}",
                        "l2": "inputs larger than L2 (1.34 GB per state buffer vs 126 MB L2)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,

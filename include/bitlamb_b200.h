@@ -62,6 +62,13 @@ typedef enum bl_variant {  /* OptimizerVariant, optimizers.hpp:30-39 */
 
 typedef enum bl_memory { BL_MEM_HOST = 0, BL_MEM_DEVICE = 1 } bl_memory;
 
+/* How NCCL-mode ranks exchange packets. */
+typedef enum bl_transport {
+  BL_TRANSPORT_AUTO = 0, /* fused NVLink peer stores when every peer maps, else NCCL */
+  BL_TRANSPORT_NCCL = 1, /* grouped ncclSend/ncclRecv alltoall + ncclAllGather */
+  BL_TRANSPORT_P2P = 2   /* fused: K1/K3 store packet words into peer HBM (CUDA IPC) */
+} bl_transport;
+
 typedef enum bl_state {  /* LayerState members, optimizers.hpp:68-78 */
   BL_STATE_X = 0,
   BL_STATE_M = 1,
@@ -84,6 +91,7 @@ typedef struct bl_cluster_config {
   double compensation_tolerance;
   const uint8_t* nccl_unique_id; /* BL_NCCL_UNIQUE_ID_BYTES, BL_MODE_NCCL only */
   void* stream;                  /* cudaStream_t; NULL = library-owned stream */
+  int32_t transport;             /* bl_transport, BL_MODE_NCCL only */
 } bl_cluster_config;
 
 /* VolumeLedger, comm_sim.hpp:37-50 */
@@ -140,6 +148,8 @@ void bl_hparams_default(bl_hparams* hp);
 bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out);
 void bl_cluster_destroy(bl_cluster* c);
 bl_status bl_cluster_dims(const bl_cluster* c, uint64_t* padded, uint64_t* chunk);
+/* The packet transport in use (bl_transport; BL_TRANSPORT_AUTO is resolved). */
+int32_t bl_cluster_transport(const bl_cluster* c);
 
 /* SimCluster::compressed_allreduce (comm_sim.hpp:98-99, comm_sim.cpp:120-203).
  * inputs[i] is worker i's stream of `len` floats (len must equal dim,

@@ -78,7 +78,7 @@ class _ClusterConfig(C.Structure):
                 ("device", C.c_int32), ("dim", C.c_uint64), ("compressor", C.c_int32),
                 ("baseline_bits_per_element", C.c_int32), ("verify_compensation", C.c_int32),
                 ("endpoint_stats", C.c_int32), ("compensation_tolerance", C.c_double),
-                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p)]
+                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("transport", C.c_int32)]
 
 
 class _Ledger(C.Structure):
@@ -116,6 +116,8 @@ def _load() -> C.CDLL:
     so.bl_cluster_create.argtypes = [C.POINTER(_ClusterConfig), C.POINTER(P)]
     so.bl_cluster_destroy.argtypes = [P]
     so.bl_cluster_dims.argtypes = [P, C.POINTER(u64), C.POINTER(u64)]
+    so.bl_cluster_transport.argtypes = [P]
+    so.bl_cluster_transport.restype = i32
     so.bl_cluster_compressed_allreduce.argtypes = [P, P, i32, u64, P, C.c_double, i32]
     so.bl_cluster_lossless_allreduce.argtypes = [P, P, i32, u64, P, i32]
     so.bl_cluster_worker_error.argtypes = [P, i32, P]
@@ -288,7 +290,8 @@ class SimCluster:
     def __init__(self, n_workers: int, dim: int, compressor: str = "onebit",
                  baseline_bits_per_element: int = 16, *, mode: str = "sim", rank: int = 0,
                  device: int = 0, nccl_unique_id: bytes | None = None, stream=None,
-                 endpoint_stats: bool = False, verify_compensation: bool = False):
+                 endpoint_stats: bool = False, verify_compensation: bool = False,
+                 transport: str = "auto"):
         cfg = _ClusterConfig()
         cfg.n_workers = n_workers
         cfg.mode = 0 if mode == "sim" else 1
@@ -305,6 +308,7 @@ class SimCluster:
             self._uid = (C.c_uint8 * 128).from_buffer_copy(nccl_unique_id)
             cfg.nccl_unique_id = C.addressof(self._uid)
         cfg.stream = stream
+        cfg.transport = {"auto": 0, "nccl": 1, "p2p": 2}[transport]
         h = C.c_void_p()
         _check(_lib.bl_cluster_create(C.byref(cfg), C.byref(h)))
         self._h = h
@@ -325,6 +329,13 @@ class SimCluster:
     @property
     def handle(self):
         return self._h
+
+    @property
+    def transport(self) -> str:
+        """'sim', 'nccl' or 'p2p' (fused NVLink peer stores)."""
+        if self.mode == "sim":
+            return "sim"
+        return {1: "nccl", 2: "p2p"}.get(int(_lib.bl_cluster_transport(self._h)), "nccl")
 
     def n_workers(self) -> int:
         return self._n

@@ -168,17 +168,33 @@ __device__ __forceinline__ uint32_t row_nibble(const uint32_t* words, int r, int
   return (__ldg(words + 4 * r + (lane >> 3)) >> (4 * (lane & 7))) & 0xFu;
 }
 
-// Pack the lane nibbles of one row into 4 packet words (LSB-first).
-__device__ __forceinline__ void store_row_bits(uint32_t* words, int r, int lane, uint32_t nib) {
+// Pack the lane nibbles of one row into 4 packet words (LSB-first); with a
+// remote slot the word is also stored into the peer's memory over NVLink.
+__device__ __forceinline__ void store_row_bits(uint32_t* words, int r, int lane, uint32_t nib,
+                                               uint32_t* remote = nullptr) {
   uint32_t v = nib << (4 * (lane & 7));
   v |= __shfl_xor_sync(FULL, v, 1);
   v |= __shfl_xor_sync(FULL, v, 2);
   v |= __shfl_xor_sync(FULL, v, 4);
-  if ((lane & 7) == 0) words[4 * r + (lane >> 3)] = v;
+  if ((lane & 7) == 0) {
+    words[4 * r + (lane >> 3)] = v;
+    if (remote) remote[4 * r + (lane >> 3)] = v;
+  }
 }
 
 __device__ __forceinline__ float slot_scale(const uint32_t* slot, uint64_t W) {
   return __uint_as_float(__ldg(slot + W));
+}
+
+// L2-coherent loads for data a peer GPU writes while the consuming kernel is
+// already resident (fused exchange): never through the non-coherent path.
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ float slot_scale_cg(const uint32_t* slot, uint64_t W) {
+  return __uint_as_float(__ldcg(slot + W));
+}
+__device__ __forceinline__ uint32_t nibble_cg(const uint32_t* sl, uint32_t i) {
+  const uint32_t w0 = __ldcg(sl + (i >> 5)), w1 = __ldcg(sl + (i >> 5) + 1);
+  return __funnelshift_r(w0, w1, i & 31u) & 0xFu;
 }
 
 // Decompressed result value of a packet bit (compression.cpp:68-81):
@@ -201,6 +217,35 @@ __device__ __forceinline__ int find_layer(const uint64_t* off, int L, uint64_t k
 
 __device__ __forceinline__ void flag(unsigned long long* err, int slot, unsigned long long key) {
   if (err) atomicMin(err + slot, key);
+}
+
+// ---- fused NVLink exchange: epoch flags in peer memory -----------------------
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Thread 0 of the block waits until flags[0..n) >= epoch (bounded: a peer that
+// never signals sets kErrPeer instead of hanging the GPU), then the block syncs.
+__device__ __forceinline__ void wait_peers(const unsigned long long* flags, int n,
+                                           unsigned long long epoch, unsigned long long* err) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n; ++i) {
+      long long spins = 0;
+      while (ld_acquire_sys(flags + i) < epoch) {
+        __nanosleep(128);
+        if (++spins > (1ll << 25)) {  // ~5 s
+          flag(err, kErrPeer, static_cast<unsigned long long>(i));
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -240,6 +285,7 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
     float* we = p.werr + ep * p.c_pad + i0;
     const uint32_t* pkp = p.pk_prev + ep * p.slot;
     uint32_t* pkc = p.pk_cur + ep * p.slot + (i0 >> 5);
+    uint32_t* rxw = p.peer_rx ? p.peer_rx[j] + p.rx_off + (i0 >> 5) : nullptr;
     const float Sp = slot_scale(pkp, p.W);
     pkp += i0 >> 5;
 
@@ -321,7 +367,7 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
             }
           }
           st4(we + (r0 + k) * kRowElems + 4 * lane, rawn);
-          store_row_bits(pkc, r0 + k, lane, nib);
+          store_row_bits(pkc, r0 + k, lane, nib, rxw);
         }
       }
       acc = warp_bfly_sum(acc);
@@ -420,7 +466,7 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
         }
       }
       st4(we + r * kRowElems + 4 * lane, rawn);
-      store_row_bits(pkc, r, lane, nib);
+      store_row_bits(pkc, r, lane, nib, rxw);
     }
     acc = warp_bfly_sum(acc);
     if (lane == 0) p.partials[ep * p.tpc + t] = acc;
@@ -429,6 +475,7 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
       if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
     }
   }
+  if (p.peer_rx) __threadfence_system();  // remote packet words before the finalize signal
 }
 
 // Scale of each endpoint: S = (float)(sum|corrected| / c) (compression.cpp:54-55),
@@ -444,6 +491,12 @@ __global__ void __launch_bounds__(1024) k_finalize_scales(const FinalizeParams p
     const float S = static_cast<float>(s / static_cast<double>(p.c));
     p.slots[static_cast<size_t>(e) * p.slot_stride + p.W] = __float_as_uint(S);
     if (!isfinite(S)) flag(p.err, kErrScale, static_cast<unsigned long long>(p.err_base + e));
+    if (p.peer_slots) {
+      const int q0 = p.to_all ? 0 : e, q1 = p.to_all ? p.n : e + 1;
+      for (int q = q0; q < q1; ++q) p.peer_slots[q][p.peer_off + p.W] = __float_as_uint(S);
+      __threadfence_system();
+      for (int q = q0; q < q1; ++q) st_release_sys(p.peer_flags[q] + p.flag_index, p.epoch);
+    }
   }
 }
 
@@ -452,6 +505,21 @@ __global__ void __launch_bounds__(1024) k_finalize_scales(const FinalizeParams p
 // n one-bit messages (compression.cpp:83-89, skipped when S == 0; scale 1/n in
 // fp64, :164), error-compensated recompression with the server residual.
 // ---------------------------------------------------------------------------
+// Allgather fused into K3: the row's 4 server words (just written to the local
+// result slot by the same warp) are copied into every peer's result slot.
+__device__ __forceinline__ void push_words(const K3Params& p, const uint32_t* rc, int r, int lane,
+                                           uint64_t i0) {
+  __syncwarp();
+  if ((lane & 7) == 0) {
+    const int wi = 4 * r + (lane >> 3);
+    const uint32_t v = rc[wi];
+    for (int q = 0; q < p.n; ++q) {
+      if (q == p.rank) continue;
+      p.peer_res[q][p.res_off + (i0 >> 5) + wi] = v;
+    }
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
   __shared__ float s_scale[kWarpsPerBlock][64];
@@ -462,6 +530,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
   const long long total = static_cast<long long>(p.ns) * p.tpc;
   const float es = p.es_dev ? __ldg(p.es_dev) : p.es_host;
   const double inv_n = 1.0 / static_cast<double>(n);
+  if (p.wait_flags) wait_peers(p.wait_flags, n, p.epoch, p.err);
 
   for (long long tile = gw; tile < total; tile += nwarps) {
     const int sv = static_cast<int>(tile / p.tpc);
@@ -470,7 +539,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
     const uint64_t i0 = static_cast<uint64_t>(t) * kTile;
     const uint32_t* in = p.in + sv * p.in_s;
     __syncwarp();
-    for (int i = lane; i < n; i += 32) s_scale[wib][i] = slot_scale(in + i * p.in_i, p.W);
+    for (int i = lane; i < n; i += 32) s_scale[wib][i] = slot_scale_cg(in + i * p.in_i, p.W);
     __syncwarp();
     float* se = p.serr + static_cast<size_t>(sv) * p.c_pad + i0;
     const uint32_t* rs = p.res_prev + static_cast<size_t>(j) * p.slot;
@@ -496,7 +565,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
           sn[k] = __ldg(rs + 4 * (r0 + k) + wsub) >> sh;
 #pragma unroll
           for (int i = 0; i < (NT > 0 ? NT : 1); ++i)
-            wn[k][i] = __ldg(inw + i * p.in_i + 4 * (r0 + k) + wsub) >> sh;
+            wn[k][i] = ld_cg(inw + i * p.in_i + 4 * (r0 + k) + wsub) >> sh;
         }
 #pragma unroll
         for (int k = 0; k < R; ++k) {
@@ -532,6 +601,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
           }
           st4(se + (r0 + k) * kRowElems + 4 * lane, rawn);
           store_row_bits(rc, r0 + k, lane, nib);
+          if (p.peer_res) push_words(p, rc, r0 + k, lane, i0);
         }
       }
       acc = warp_bfly_sum(acc);
@@ -554,7 +624,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
 #pragma unroll(NT > 0 ? NT : 1)
       for (int i = 0; i < n; ++i) {
         const float S = s_scale[wib][i];
-        const uint32_t nb = row_nibble(inw + i * p.in_i, r, lane);
+        const uint32_t nb = (ld_cg(inw + i * p.in_i + 4 * r + (lane >> 3)) >> (4 * (lane & 7))) & 0xFu;
         if (S != 0.0f) {
           const double Sd = S;
           a0 += (nb & 1u) ? Sd : -Sd;
@@ -586,6 +656,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
       }
       st4(se + r * kRowElems + 4 * lane, rawn);
       store_row_bits(rc, r, lane, nib);
+      if (p.peer_res) push_words(p, rc, r, lane, i0);
     }
     acc = warp_bfly_sum(acc);
     if (lane == 0) p.partials[static_cast<size_t>(sv) * p.tpc + t] = acc;
@@ -594,6 +665,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
       if (lane == 0) p.cmax[static_cast<size_t>(sv) * p.tpc + t] = cm;
     }
   }
+  if (p.peer_res) __threadfence_system();  // remote server words before the finalize signal
 }
 
 // Result bits of 4 consecutive global elements k0..k0+3 from chunk-relative
@@ -609,8 +681,8 @@ __device__ __forceinline__ uint32_t bit_at(const BitCursor& bc, uint64_t k, floa
   if (j >= static_cast<uint64_t>(bc.n)) j = bc.n - 1;
   const uint64_t i = k - j * bc.c;
   const uint32_t* sl = bc.res + j * bc.slot;
-  *S = slot_scale(sl, bc.W);
-  return (__ldg(sl + (i >> 5)) >> (i & 31)) & 1u;
+  *S = slot_scale_cg(sl, bc.W);
+  return (__ldcg(sl + (i >> 5)) >> (i & 31)) & 1u;
 }
 
 // Values m_g = dec * invc for the lane's 4 elements of a layer row starting at
@@ -624,11 +696,11 @@ __device__ __forceinline__ float4 row_mg(const BitCursor& bc, uint64_t kr, int l
   float4 out;
   if (kr + (kRowElems - 1) < chunk_end || j + 1 >= static_cast<uint64_t>(bc.n)) {
     const uint32_t* sl = bc.res + j * bc.slot;
-    const float S = slot_scale(sl, bc.W);
+    const float S = slot_scale_cg(sl, bc.W);
     const float pos = S, neg = S == 0.0f ? 0.0f : -S;
     const uint64_t i = kr - j * bc.c + 4 * lane;
     const uint64_t wi = i >> 5;
-    const uint32_t w0 = __ldg(sl + wi), w1 = __ldg(sl + wi + 1);
+    const uint32_t w0 = __ldcg(sl + wi), w1 = __ldcg(sl + wi + 1);
     const uint32_t nib = __funnelshift_r(w0, w1, static_cast<uint32_t>(i & 31)) & 0xFu;
     out.x = __fmul_rn(nib & 1u ? pos : neg, ic);
     out.y = __fmul_rn(nib & 2u ? pos : neg, ic);
@@ -668,6 +740,7 @@ __device__ __forceinline__ int lane_valid(uint64_t len, uint64_t ir, int lane) {
 // ---------------------------------------------------------------------------
 template <int MPREV>
 __global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
+  if (p.wait_flags) wait_peers(p.wait_flags, p.n, p.epoch, p.err);
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -690,7 +763,7 @@ __global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
       // Fast path: aligned, full tile, one chunk of the result.
       constexpr int R = 4;
       const uint32_t* sl = cur.res + j * p.slot;
-      const float S = slot_scale(sl, p.W);
+      const float S = slot_scale_cg(sl, p.W);
       const float pos = S, neg = S == 0.0f ? 0.0f : -S;
       const uint32_t* slp = MPREV ? prv.res + j * p.slot : nullptr;
       float posp = 0.f, negp = 0.f;
@@ -711,7 +784,7 @@ __global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
           const float* row = p.v + base + (r0 + k) * kRowElems + 4 * lane;
           v[k] = ldg_rw(row);
           vf[k] = ldg_ro(p.vf + base + (r0 + k) * kRowElems + 4 * lane);
-          nc[k] = nibble_at(sl, ib + (r0 + k) * kRowElems);
+          nc[k] = nibble_cg(sl, ib + (r0 + k) * kRowElems);
           if (MPREV) np[k] = nibble_at(slp, ib + (r0 + k) * kRowElems);
           else mpb[k] = ldg_ro(p.m + base + (r0 + k) * kRowElems + 4 * lane);
         }
@@ -1225,6 +1298,12 @@ __global__ void __launch_bounds__(1024) k_error_stats_final(const double* part, 
 
 __global__ void k_set_float(float* p, float v) { *p = v; }
 
+// Stream-ordered wait for n peer signals (fused NVLink exchange).
+__global__ void k_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
+                             unsigned long long* err) {
+  wait_peers(flags, n, epoch, err);
+}
+
 __global__ void k_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const float* m,
                                const uint64_t* off, int L, const float* A, const float* B,
                                unsigned long long* err, int worker_base) {
@@ -1363,6 +1442,12 @@ int launch_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const fl
                         const uint64_t* off, int L, const float* A, const float* B,
                         unsigned long long* err, int worker_base, cudaStream_t s) {
   k_build_stream<<<grid_for_elems(d), 256, 0, s>>>(in, stride, nw, d, m, off, L, A, B, err, worker_base);
+  return 1;
+}
+
+int launch_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
+                      unsigned long long* err, cudaStream_t s) {
+  k_wait_peers<<<1, 32, 0, s>>>(flags, n, epoch, err);
   return 1;
 }
 

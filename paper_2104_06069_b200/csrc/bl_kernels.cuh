@@ -25,6 +25,7 @@ enum ErrSlot : int {
   kErrGrad = 0,    // non-finite gradient: key = worker << 40 | element
   kErrScale = 1,   // non-finite compression scale: key = endpoint id
   kErrRecon = 2,   // non-finite reconstructed gradient: key = layer
+  kErrPeer = 3,    // peer signal timeout (fused NVLink exchange): key = peer rank
   kErrSlots = 4,
 };
 
@@ -56,6 +57,10 @@ struct K1Params {
   float* cmax;                // [nw][n][tpc] max|corrected| per tile (stats) or nullptr
   unsigned long long* err;
   int worker_base;            // global worker id of local worker 0
+  // Fused NVLink exchange (NCCL-mode P2P transport): the words of chunk j are
+  // also stored into rank j's receive slot peer_rx[j] + rx_off.
+  uint32_t* const* peer_rx;   // [n] peer receive-buffer bases (nullptr: no fused exchange)
+  uint64_t rx_off;            // word offset of this rank's slot in the current parity
 };
 
 // K3: server reduction of chunk(s) owned locally.
@@ -74,6 +79,14 @@ struct K3Params {
   float es_host;
   double* partials;           // [ns][tpc]
   float* cmax;                // [ns][tpc] or nullptr
+  // Fused NVLink exchange: wait for every worker's packet, then store the
+  // server words into every peer's result slot peer_res[q] + res_off.
+  const unsigned long long* wait_flags;  // [n] local worker flags or nullptr
+  unsigned long long epoch;
+  uint32_t* const* peer_res;  // [n] peer result-buffer bases or nullptr
+  uint64_t res_off;
+  int rank;
+  unsigned long long* err;
 };
 
 struct FinalizeParams {
@@ -84,6 +97,16 @@ struct FinalizeParams {
   uint64_t slot_stride, W;
   unsigned long long* err;
   int err_base;            // key offset for kErrScale
+  // Fused NVLink exchange: endpoint e's scale also goes to peer_slots[q] + peer_off
+  // (q = e for worker packets, every q for the server packet), then the flag
+  // peer_flags[q][flag_index] is raised to `epoch` (release, system scope).
+  uint32_t* const* peer_slots;
+  uint64_t peer_off;
+  unsigned long long* const* peer_flags;
+  int flag_index;
+  int to_all;
+  int n;
+  unsigned long long epoch;
 };
 
 // Layer-tiled kernels (K5, K6, W1, W2).
@@ -112,6 +135,8 @@ struct K5Params {
   const float* dense;        // identity compressor: dense result (m_g = dense * invc)
   float* m_store;            // identity compressor: m <- m_g
   int norm_only;             // lamb_basic_1bit / onebit_adam: only ||v||^2 partials
+  const unsigned long long* wait_flags;  // [n] server flags (fused exchange) or nullptr
+  unsigned long long epoch;
 };
 
 struct EpiParams {
@@ -211,6 +236,9 @@ int launch_error_stats(const float* raw, uint64_t c_pad, const uint32_t* pk, uin
                        uint64_t W, uint64_t c, uint64_t len, double* scratch, int scratch_tiles,
                        float* scratch_max, double* out, cudaStream_t s);
 int launch_set_float(float* p, float v, cudaStream_t s);
+// Block the stream until flags[0..n) >= epoch (peer signals, bounded wait).
+int launch_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
+                      unsigned long long* err, cudaStream_t s);
 // Identity-compressor stream build in place (optimizers.cpp:248-255):
 // in[w][k] = A_l*m[k] + B_l*in[w][k] for k < d, with the gradient finite check.
 int launch_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const float* m,

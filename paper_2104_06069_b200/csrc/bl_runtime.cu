@@ -163,17 +163,39 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
   p.cmax = cfg.endpoint_stats ? wcmax : nullptr;
   p.err = err;
   p.worker_base = mode == BL_MODE_SIM ? 0 : rank;
+  const bool p2p = transport == BL_TRANSPORT_P2P;
+  const unsigned long long epoch = calls + 1;
+  const uint64_t my_slot = (static_cast<uint64_t>(cur()) * n + rank) * slot;
+  if (p2p) {
+    p.peer_rx = d_peer_rx;  // fused alltoall: K1 stores chunk j's words into rank j's rx
+    p.rx_off = my_slot;
+  }
   cudaEvent_t a;
   begin(KC_K1, &a);
   end(KC_K1, a, launch_k1(p, k1_mode, grid(static_cast<long long>(nw) * n * tpc), stream));
 
   FinalizeParams f{wpart, tpc, c, wpk[cur()], slot, W, err, p.worker_base * n};
+  if (p2p) {
+    f.peer_slots = d_peer_rx;
+    f.peer_off = my_slot;
+    f.peer_flags = d_peer_flags;
+    f.flag_index = rank;
+    f.to_all = 0;
+    f.n = n;
+    f.epoch = epoch;
+  }
   begin(KC_FIN, &a);
   end(KC_FIN, a, launch_finalize(f, nw * n, stream));
 
   const uint32_t* kin = wpk[cur()];
   uint64_t in_s = slot, in_i = static_cast<uint64_t>(n) * slot;
-  if (mode == BL_MODE_NCCL) {
+  if (p2p) {
+    begin(KC_A2A, &a);
+    end(KC_A2A, a, launch_wait_peers(flags, n, epoch, err, stream));
+    kin = rx + static_cast<size_t>(cur()) * n * slot;
+    in_s = 0;
+    in_i = slot;
+  } else if (mode == BL_MODE_NCCL) {
     begin(KC_A2A, &a);
     const size_t words = W + 1;  // sign words + scale word
     cuda_check(cudaMemcpyAsync(rpk + static_cast<size_t>(rank) * slot,
@@ -215,15 +237,33 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
   k3.es_host = es_host;
   k3.partials = spart;
   k3.cmax = cfg.endpoint_stats ? scmax : nullptr;
+  k3.err = err;
+  if (p2p) {
+    k3.peer_res = d_peer_res;  // fused allgather: server words into every peer's result slot
+    k3.res_off = my_slot;
+    k3.rank = rank;
+  }
   begin(KC_K3, &a);
   end(KC_K3, a, launch_k3(k3, grid(static_cast<long long>(ns) * tpc), stream));
 
   FinalizeParams f2{spart, tpc, c, res[cur()] + static_cast<size_t>(k3.server_base) * slot, slot,
                     W, err, 1 << 20};
+  if (p2p) {
+    f2.peer_slots = d_peer_res;
+    f2.peer_off = my_slot;
+    f2.peer_flags = d_peer_flags;
+    f2.flag_index = n + rank;
+    f2.to_all = 1;
+    f2.n = n;
+    f2.epoch = epoch;
+  }
   begin(KC_FIN, &a);
   end(KC_FIN, a, launch_finalize(f2, ns, stream));
 
-  if (mode == BL_MODE_NCCL && n > 1) {
+  if (p2p) {
+    begin(KC_AG, &a);
+    end(KC_AG, a, launch_wait_peers(flags + n, n, epoch, err, stream));
+  } else if (mode == BL_MODE_NCCL && n > 1) {
     begin(KC_AG, &a);
     nccl_check(ncclAllGather(res[cur()] + static_cast<size_t>(rank) * slot, res[cur()], slot,
                              ncclUint32, comm, stream),
@@ -234,6 +274,76 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
   last_identity = false;
   ledger_compressed();
   if (cfg.endpoint_stats) refresh_stats();
+}
+
+// Map every peer's receive buffer, result buffer and flag words into this
+// process (CUDA IPC over NVLink).  Collective: every rank takes the same
+// decision (NCCL min-reduce of the per-rank success bit).
+void bl_cluster::setup_p2p(bool required) {
+  const size_t nn = static_cast<size_t>(n);
+  rx = dalloc<uint32_t>(2 * nn * slot);
+  flags = reinterpret_cast<unsigned long long*>(dalloc<double>(2 * nn));
+  constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
+  std::vector<uint8_t> mine(3 * kH);
+  cudaIpcMemHandle_t h[3];
+  cuda_check(cudaIpcGetMemHandle(&h[0], rx), "cudaIpcGetMemHandle(rx)");
+  cuda_check(cudaIpcGetMemHandle(&h[1], res_base), "cudaIpcGetMemHandle(res)");
+  cuda_check(cudaIpcGetMemHandle(&h[2], flags), "cudaIpcGetMemHandle(flags)");
+  std::memcpy(mine.data(), h, 3 * kH);
+  uint8_t* dbuf = reinterpret_cast<uint8_t*>(dalloc<double>((nn * 3 * kH + 7) / 8 + 1));
+  cuda_check(cudaMemcpy(dbuf + static_cast<size_t>(rank) * 3 * kH, mine.data(), 3 * kH,
+                        cudaMemcpyHostToDevice),
+             "handle upload");
+  nccl_check(ncclAllGather(dbuf + static_cast<size_t>(rank) * 3 * kH, dbuf, 3 * kH, ncclUint8, comm,
+                           stream),
+             "ncclAllGather(handles)");
+  std::vector<uint8_t> all(nn * 3 * kH);
+  cuda_check(cudaMemcpyAsync(all.data(), dbuf, all.size(), cudaMemcpyDeviceToHost, stream), "handles");
+  cuda_check(cudaStreamSynchronize(stream), "handles sync");
+  std::vector<void*> prx(nn), pres(nn), pfl(nn);
+  int ok = 1;
+  for (int q = 0; q < n; ++q) {
+    if (q == rank) {
+      prx[q] = rx;
+      pres[q] = res_base;
+      pfl[q] = flags;
+      continue;
+    }
+    void* ptrs[3] = {nullptr, nullptr, nullptr};
+    for (int k = 0; k < 3 && ok; ++k) {
+      cudaIpcMemHandle_t hq;
+      std::memcpy(&hq, all.data() + (static_cast<size_t>(q) * 3 + k) * kH, kH);
+      if (cudaIpcOpenMemHandle(&ptrs[k], hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+      } else {
+        ipc_opened.push_back(ptrs[k]);
+      }
+    }
+    prx[q] = ptrs[0];
+    pres[q] = ptrs[1];
+    pfl[q] = ptrs[2];
+  }
+  int* dok = reinterpret_cast<int*>(dbuf);
+  cuda_check(cudaMemcpy(dok, &ok, sizeof ok, cudaMemcpyHostToDevice), "ok upload");
+  nccl_check(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, comm, stream), "ncclAllReduce(ok)");
+  cuda_check(cudaMemcpyAsync(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost, stream), "ok");
+  cuda_check(cudaStreamSynchronize(stream), "ok sync");
+  cudaFree(dbuf);
+  if (!ok) {
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    ipc_opened.clear();
+    if (required) fail(BL_ERR_UNSUPPORTED, "P2P transport: a peer's memory could not be mapped");
+    transport = BL_TRANSPORT_NCCL;
+    return;
+  }
+  d_peer_rx = reinterpret_cast<uint32_t**>(dalloc<double>(nn));
+  d_peer_res = reinterpret_cast<uint32_t**>(dalloc<double>(nn));
+  d_peer_flags = reinterpret_cast<unsigned long long**>(dalloc<double>(nn));
+  cuda_check(cudaMemcpy(d_peer_rx, prx.data(), nn * sizeof(void*), cudaMemcpyHostToDevice), "tables");
+  cuda_check(cudaMemcpy(d_peer_res, pres.data(), nn * sizeof(void*), cudaMemcpyHostToDevice), "tables");
+  cuda_check(cudaMemcpy(d_peer_flags, pfl.data(), nn * sizeof(void*), cudaMemcpyHostToDevice), "tables");
+  transport = BL_TRANSPORT_P2P;
 }
 
 void bl_cluster::lossless(bool check_finite) {
@@ -342,6 +452,11 @@ void bl_cluster::check_errors(const std::vector<uint64_t>* off) {
     fail(BL_ERR_RUNTIME, buf);
   }
   if (e[kErrScale] != none) fail(BL_ERR_INVALID_ARGUMENT, "compress: input vector is not finite");
+  if (e[kErrPeer] != none) {
+    std::snprintf(buf, sizeof buf, "fused NVLink exchange: rank %llu never signalled (timeout)",
+                  e[kErrPeer]);
+    fail(BL_ERR_NCCL, buf);
+  }
   if (e[kErrRecon] != none) {  // optimizers.cpp:288-293
     std::snprintf(buf, sizeof buf, "non-finite reconstructed gradient for layer 'layer%llu'",
                   e[kErrRecon]);
@@ -705,8 +820,9 @@ bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
       c->wpk[0] = dalloc<uint32_t>(nw * n * c->slot);
       c->wpk[1] = dalloc<uint32_t>(nw * n * c->slot);
       c->serr = dalloc<float>(static_cast<size_t>(c->ns) * c->c_pad + 256);
-      c->res[0] = dalloc<uint32_t>(n * c->slot);
-      c->res[1] = dalloc<uint32_t>(n * c->slot);
+      c->res_base = dalloc<uint32_t>(2 * n * c->slot);
+      c->res[0] = c->res_base;
+      c->res[1] = c->res_base + n * c->slot;
       c->wpart = dalloc<double>(nw * n * c->tpc);
       c->spart = dalloc<double>(static_cast<size_t>(c->ns) * c->tpc);
       c->out = dalloc<float>(c->P + kSlack);
@@ -727,6 +843,9 @@ bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
         ncclUniqueId id;
         std::memcpy(id.internal, cfg->nccl_unique_id, BL_NCCL_UNIQUE_ID_BYTES);
         nccl_check(ncclCommInitRank(&c->comm, c->n, id, c->rank), "ncclCommInitRank");
+        if (c->n > 1 && cfg->transport != BL_TRANSPORT_NCCL) {
+          c->setup_p2p(cfg->transport == BL_TRANSPORT_P2P);
+        }
       }
       cuda_check(cudaDeviceSynchronize(), "cluster init");
     } catch (...) {
@@ -741,10 +860,13 @@ void bl_cluster_destroy(bl_cluster* c) {
   if (!c) return;
   DeviceGuard g(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->comm) ncclCommDestroy(c->comm);
-  void* bufs[] = {c->in,    c->werr,  c->wpk[0], c->wpk[1],    c->rpk,      c->serr,
-                  c->res[0], c->res[1], c->wpart, c->spart,    c->wcmax,    c->scmax,
-                  c->out,   c->lrecv, c->err,    c->stat_part, c->stat_max, c->stat_out};
+  void* bufs[] = {c->in,        c->werr,       c->wpk[0],          c->wpk[1],    c->rpk,
+                  c->serr,      c->res_base,   c->wpart,           c->spart,     c->wcmax,
+                  c->scmax,     c->out,        c->lrecv,           c->err,       c->stat_part,
+                  c->stat_max,  c->stat_out,   c->rx,              c->flags,     c->d_peer_rx,
+                  c->d_peer_res, c->d_peer_flags};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& e : c->pending) {
@@ -755,6 +877,8 @@ void bl_cluster_destroy(bl_cluster* c) {
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
+
+int32_t bl_cluster_transport(const bl_cluster* c) { return c ? c->transport : BL_TRANSPORT_NCCL; }
 
 bl_status bl_cluster_dims(const bl_cluster* c, uint64_t* padded, uint64_t* chunk) {
   return guarded([&] {

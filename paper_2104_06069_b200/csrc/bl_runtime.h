@@ -79,6 +79,17 @@ struct bl_cluster {
   double* stat_out = nullptr;   // [2]
   int stat_tiles = 0;
 
+  // Fused NVLink exchange (BL_TRANSPORT_P2P): CUDA-IPC-mapped peer buffers.
+  int transport = BL_TRANSPORT_NCCL;
+  uint32_t* res_base = nullptr;       // one allocation: res[0] | res[1]
+  uint32_t* rx = nullptr;             // [2][n][slot] worker packets addressed to this rank
+  unsigned long long* flags = nullptr;  // [2n]: worker-packet flags, server-packet flags
+  uint32_t** d_peer_rx = nullptr;     // [n] device table of peers' rx
+  uint32_t** d_peer_res = nullptr;    // [n] device table of peers' res_base
+  unsigned long long** d_peer_flags = nullptr;  // [n]
+  std::vector<void*> ipc_opened;
+  void setup_p2p(bool required);
+
   uint64_t calls = 0;           // compressed collectives run (ping-pong index)
   bool last_identity = false;
   bl_volume_ledger ledger{};

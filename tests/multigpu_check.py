@@ -49,9 +49,12 @@ def main() -> int:
         if not cond:
             failures.append(what)
 
+    transports = sys.argv[1:] or ["p2p", "nccl"]
     # ---- 1. compressed_allreduce API: real vs sim --------------------------
-    for d in (37, 10001, 4096 * 5 + 3, 1_000_003):
-        cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid())
+    for tp, d in [(tp, d) for tp in transports for d in (37, 10001, 4096 * 5 + 3, 1_000_003)]:
+        cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid(),
+                           transport=tp)
+        check(cl.transport == tp, f"transport {cl.transport} != {tp}")
         sim = bl.SimCluster(world, d, device=local) if rank == 0 else None
         rng = np.random.default_rng(d)
         for step in range(3):
@@ -66,7 +69,7 @@ def main() -> int:
             if rank == 0:
                 ref = sim.compressed_allreduce(x, error_scale=es)
                 for r in range(world):
-                    check(outs[r] == ref.tobytes(), f"d={d} step={step} result rank {r}")
+                    check(outs[r] == ref.tobytes(), f"{tp} d={d} step={step} result rank {r}")
                     check(pk[r] == b"".join(sim.packet(r, j) for j in range(world)),
                           f"d={d} step={step} worker packets rank {r}")
                     check(sp[r] == sim.server_packet(r), f"d={d} step={step} server packet {r}")
@@ -85,12 +88,29 @@ def main() -> int:
             sim.close()
 
     # ---- 2. optimizer: warmup + freeze + compression stage -----------------
+    for tp in transports:
+        optimizer_check(rank, world, local, new_uid, check, tp)
+
+    ok = torch.tensor([0 if failures else 1], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(("MULTIGPU PASS" if ok.item() else "MULTIGPU FAIL") + f" world={world} "
+              f"transports={transports}", flush=True)
+    if failures:
+        print(f"rank {rank} failures: {failures[:10]}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0 if ok.item() else 1
+
+
+def optimizer_check(rank, world, local, new_uid, check, tp):
     sizes = [3000, 2, 1024, 1023, 5000, 3, 4096 * 3 + 17, 77777]
     d = sum(sizes)
     steps, warm = 16, 5
     hp = bl.HyperParams(total_steps=steps, warmup_steps=warm, weight_decay=0.01,
                         scaled_error_feedback=True)
-    cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid())
+    cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid(),
+                       transport=tp)
     opt = bl.Optimizer("onebit_lamb", sizes, hp, cl)
     if rank == 0:
         sim = bl.SimCluster(world, d, device=local)
@@ -110,24 +130,16 @@ def main() -> int:
             st = sopt.step(g, t, 1e-3)
             ref_x = sopt.get("x").tobytes()
             for r in range(world):
-                check(xs[r] == ref_x, f"optimizer x rank {r} t={t}")
+                check(xs[r] == ref_x, f"{tp} optimizer x rank {r} t={t}")
                 check(trs[r] == st.c.tobytes() + st.r.tobytes() + st.v_norm.tobytes(),
                       f"optimizer trace rank {r} t={t}")
     for k in ("m", "v", "v_frozen"):
         vals = gather_bytes(opt.get(k).tobytes())
         if rank == 0:
             ref = sopt.get(k).tobytes()
-            check(all(v == ref for v in vals), f"optimizer {k}")
-
-    ok = torch.tensor([0 if failures else 1], device="cuda")
-    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-    if rank == 0:
-        print(("MULTIGPU PASS" if ok.item() else "MULTIGPU FAIL") + f" world={world}", flush=True)
-    if failures:
-        print(f"rank {rank} failures: {failures[:10]}", flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
-    return 0 if ok.item() else 1
+            check(all(v == ref for v in vals), f"{tp} optimizer {k}")
+    opt.close()
+    cl.close()
 
 
 if __name__ == "__main__":
