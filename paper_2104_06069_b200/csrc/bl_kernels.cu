@@ -170,8 +170,8 @@ __device__ __forceinline__ uint32_t row_nibble(const uint32_t* words, int r, int
 
 // Pack the lane nibbles of one row into 4 packet words (LSB-first); with a
 // remote slot the word is also stored into the peer's memory over NVLink.
-__device__ __forceinline__ void store_row_bits(uint32_t* words, int r, int lane, uint32_t nib,
-                                               uint32_t* remote = nullptr) {
+__device__ __forceinline__ uint32_t store_row_bits(uint32_t* words, int r, int lane, uint32_t nib,
+                                                   uint32_t* remote = nullptr) {
   uint32_t v = nib << (4 * (lane & 7));
   v |= __shfl_xor_sync(FULL, v, 1);
   v |= __shfl_xor_sync(FULL, v, 2);
@@ -180,6 +180,23 @@ __device__ __forceinline__ void store_row_bits(uint32_t* words, int r, int lane,
     words[4 * r + (lane >> 3)] = v;
     if (remote) remote[4 * r + (lane >> 3)] = v;
   }
+  return v;
+}
+
+// Copy a finished tile's 128 packet words (512 B, just written locally by
+// this warp) to a peer slot with one 16-byte store per lane: whole NVLink
+// packets instead of scattered 4-byte writes.
+__device__ __forceinline__ void push_tile(const uint32_t* local, uint32_t* remote, int lane) {
+  __syncwarp();
+  const uint4 v = __ldcg(reinterpret_cast<const uint4*>(local) + lane);
+  reinterpret_cast<uint4*>(remote)[lane] = v;
+}
+
+// Make this warp's remote (peer-memory) stores visible system-wide before the
+// stream's next kernel raises the peer flag: warp barrier, then one fence.
+__device__ __forceinline__ void warp_fence_system(int lane) {
+  __syncwarp();
+  if (lane == 0) __threadfence_system();
 }
 
 __device__ __forceinline__ float slot_scale(const uint32_t* slot, uint64_t W) {
@@ -367,7 +384,7 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
             }
           }
           st4(we + (r0 + k) * kRowElems + 4 * lane, rawn);
-          store_row_bits(pkc, r0 + k, lane, nib, rxw);
+          store_row_bits(pkc, r0 + k, lane, nib);
         }
       }
       acc = warp_bfly_sum(acc);
@@ -376,6 +393,7 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
         cm = warp_max(cm);
         if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
       }
+      if (rxw) push_tile(pkc, rxw, lane);  // fused alltoall
       continue;
     }
 
@@ -466,7 +484,7 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
         }
       }
       st4(we + r * kRowElems + 4 * lane, rawn);
-      store_row_bits(pkc, r, lane, nib, rxw);
+      store_row_bits(pkc, r, lane, nib);
     }
     acc = warp_bfly_sum(acc);
     if (lane == 0) p.partials[ep * p.tpc + t] = acc;
@@ -474,8 +492,9 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
       cm = warp_max(cm);
       if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
     }
+    if (rxw) push_tile(pkc, rxw, lane);
   }
-  if (p.peer_rx) __threadfence_system();  // remote packet words before the finalize signal
+  if (p.peer_rx) warp_fence_system(threadIdx.x & 31);  // remote words before the finalize signal
 }
 
 // Scale of each endpoint: S = (float)(sum|corrected| / c) (compression.cpp:54-55),
@@ -507,23 +526,24 @@ __global__ void __launch_bounds__(1024) k_finalize_scales(const FinalizeParams p
 // ---------------------------------------------------------------------------
 // Allgather fused into K3: the row's 4 server words (just written to the local
 // result slot by the same warp) are copied into every peer's result slot.
-__device__ __forceinline__ void push_words(const K3Params& p, const uint32_t* rc, int r, int lane,
-                                           uint64_t i0) {
+__device__ __forceinline__ void push_all(const K3Params& p, uint32_t* const* peers,
+                                         const uint32_t* rc, uint64_t i0, int lane) {
   __syncwarp();
-  if ((lane & 7) == 0) {
-    const int wi = 4 * r + (lane >> 3);
-    const uint32_t v = rc[wi];
-    for (int q = 0; q < p.n; ++q) {
-      if (q == p.rank) continue;
-      p.peer_res[q][p.res_off + (i0 >> 5) + wi] = v;
-    }
+  const uint4 v = __ldcg(reinterpret_cast<const uint4*>(rc) + lane);
+  for (int q = 0; q < p.n; ++q) {
+    if (q != p.rank) reinterpret_cast<uint4*>(peers[q] + p.res_off + (i0 >> 5))[lane] = v;
   }
 }
 
 template <int NT>
 __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
   __shared__ float s_scale[kWarpsPerBlock][64];
+  __shared__ uint32_t* s_peer[64];
   const int n = NT > 0 ? NT : p.n;
+  if (p.peer_res) {
+    for (int q = threadIdx.x; q < p.n; q += blockDim.x) s_peer[q] = p.peer_res[q];
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -601,7 +621,6 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
           }
           st4(se + (r0 + k) * kRowElems + 4 * lane, rawn);
           store_row_bits(rc, r0 + k, lane, nib);
-          if (p.peer_res) push_words(p, rc, r0 + k, lane, i0);
         }
       }
       acc = warp_bfly_sum(acc);
@@ -610,6 +629,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
         cm = warp_max(cm);
         if (lane == 0) p.cmax[static_cast<size_t>(sv) * p.tpc + t] = cm;
       }
+      if (p.peer_res) push_all(p, s_peer, rc, i0, lane);  // fused allgather
       continue;
     }
 
@@ -656,7 +676,6 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
       }
       st4(se + r * kRowElems + 4 * lane, rawn);
       store_row_bits(rc, r, lane, nib);
-      if (p.peer_res) push_words(p, rc, r, lane, i0);
     }
     acc = warp_bfly_sum(acc);
     if (lane == 0) p.partials[static_cast<size_t>(sv) * p.tpc + t] = acc;
@@ -664,8 +683,9 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
       cm = warp_max(cm);
       if (lane == 0) p.cmax[static_cast<size_t>(sv) * p.tpc + t] = cm;
     }
+    if (p.peer_res) push_all(p, s_peer, rc, i0, lane);
   }
-  if (p.peer_res) __threadfence_system();  // remote server words before the finalize signal
+  if (p.peer_res) warp_fence_system(lane);  // remote server words before the finalize signal
 }
 
 // Result bits of 4 consecutive global elements k0..k0+3 from chunk-relative
