@@ -112,6 +112,7 @@ class SimCluster {
     bool endpoint_stats = false;
     int device = 0;
     void* stream = nullptr;
+    bl_transport transport = BL_TRANSPORT_AUTO;  // NCCL mode: fused NVLink or NCCL
   };
 
   // n_workers simulated ranks in one GPU's HBM (the reference's SimCluster).
@@ -208,6 +209,7 @@ class SimCluster {
     c.endpoint_stats = cfg.endpoint_stats ? 1 : 0;
     c.compensation_tolerance = 1e-12;
     c.stream = cfg.stream;
+    c.transport = cfg.transport;
     return c;
   }
   void fill_dims() {
