@@ -323,14 +323,21 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
     // accumulation order as the general path below.
     bool fast = MODE != 1 && i0 + kTile <= p.c && kc + i0 + kTile <= p.d;
     if (fast && MODE == 2) {
-      const int l0 = find_layer(p.off, p.L, kc + i0);
-      fast = l0 < p.L && kc + i0 + (kTile - 1) < __ldg(p.off + l0 + 1);
+      int l0;
+      if (p.tile_layer) {
+        l0 = __ldg(p.tile_layer + static_cast<size_t>(j) * p.tpc + t);
+        fast = l0 >= 0;
+      } else {
+        l0 = find_layer(p.off, p.L, kc + i0);
+        fast = l0 < p.L && kc + i0 + (kTile - 1) < __ldg(p.off + l0 + 1);
+      }
       if (fast) {
         A = __ldg(p.A + l0);
         B = __ldg(p.B + l0);
         IC = __ldg(p.invc + l0);
       }
     }
+    if (fast && p.skip_fast) continue;  // done by k1_bulk
     if (fast) {
       constexpr int R = 4;
       const uint32_t sh = 4 * (lane & 7);
@@ -495,6 +502,246 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
     if (rxw) push_tile(pkc, rxw, lane);
   }
   if (p.peer_rx) warp_fence_system(threadIdx.x & 31);  // remote words before the finalize signal
+}
+
+// ---------------------------------------------------------------------------
+// K1 bulk: the fast tiles of K1 with the operand rows staged in shared memory
+// by the bulk-copy (TMA) engine.  Each warp owns a 3-stage ring; a stage is 4
+// rows of g (read from the 16-byte-aligned address below the row start, so
+// misaligned chunks cost nothing extra), 4 rows of werr and the packet words
+// of those rows, completed on an mbarrier.  Registers hold only compute state,
+// so 2 batches per warp stay in flight.  Same arithmetic and accumulation
+// order as the fast path of k1_worker_compress.
+// ---------------------------------------------------------------------------
+constexpr int kBulkWarps = 4;
+constexpr int kBulkStages = 3;
+constexpr int kBulkR = 4;
+constexpr int kBulkG = (kBulkR * kRowElems + 4) * 4;  // 2064 B
+constexpr int kBulkW = kBulkR * kRowElems * 4;        // 2048 B
+constexpr int kBulkBits = kBulkR * 4 * 4;             // 64 B
+constexpr int kBulkStage = kBulkG + kBulkW + 2 * kBulkBits;
+constexpr int kBulkSmem = kBulkWarps * kBulkStages * kBulkStage;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// Bounded wait (a lost completion must never wedge the GPU): gives up after
+// ~2^28 polls, which the parity tests would then catch as wrong output.
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  for (uint32_t it = 0; it < (1u << 28); ++it) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+  }
+}
+
+__device__ __forceinline__ float4 lds_mis(const float* p, int s) {
+  if (s == 0) return *reinterpret_cast<const float4*>(p);
+  if (s == 2) {
+    const float2 a = *reinterpret_cast<const float2*>(p), b = *reinterpret_cast<const float2*>(p + 2);
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  const float2 m = *reinterpret_cast<const float2*>(p + 1);
+  return make_float4(p[0], m.x, m.y, p[3]);
+}
+
+template <int MODE>
+__device__ __forceinline__ int k1_fast_layer(const K1Params& p, int j, int t) {
+  const uint64_t i0 = static_cast<uint64_t>(t) * kTile, kc = static_cast<uint64_t>(j) * p.c;
+  if (i0 + kTile > p.c || kc + i0 + kTile > p.d) return -1;
+  if (MODE == 0) return 0;
+  return __ldg(p.tile_layer + static_cast<size_t>(j) * p.tpc + t);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kBulkWarps * 32) k1_bulk(const K1Params p) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) unsigned long long bars[kBulkWarps][kBulkStages];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* wsm = sm + wib * kBulkStages * kBulkStage;
+  const long long gw = static_cast<long long>(blockIdx.x) * kBulkWarps + wib;
+  const long long nwarps = static_cast<long long>(gridDim.x) * kBulkWarps;
+  const long long per_w = static_cast<long long>(p.n) * p.tpc;
+  const long long total = per_w * p.nw;
+  const float es = p.es_dev ? __ldg(p.es_dev) : p.es_host;
+  if (lane == 0) {
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[wib][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  auto is_fast = [&](long long tile) {
+    const int w = static_cast<int>(tile / per_w);
+    const long long rem = tile - w * per_w;
+    const int j = static_cast<int>(rem / p.tpc);
+    return k1_fast_layer<MODE>(p, j, static_cast<int>(rem - static_cast<long long>(j) * p.tpc)) >= 0;
+  };
+  auto next_fast = [&](long long tile) {
+    while (tile < total && !is_fast(tile)) tile += nwarps;
+    return tile;
+  };
+  // Producer: lane 0 issues the copies of batch (tile, r0) into `stage`.
+  auto issue = [&](int stage, long long tile, int r0) {
+    if (tile >= total || lane != 0) return;
+    const int w = static_cast<int>(tile / per_w);
+    const long long rem = tile - w * per_w;
+    const int j = static_cast<int>(rem / p.tpc);
+    const int t = static_cast<int>(rem - static_cast<long long>(j) * p.tpc);
+    const uint64_t i0 = static_cast<uint64_t>(t) * kTile, kc = static_cast<uint64_t>(j) * p.c;
+    const size_t ep = static_cast<size_t>(w) * p.n + j;
+    const int s = static_cast<int>(kc & 3u);
+    unsigned char* st = wsm + stage * kBulkStage;
+    unsigned long long* bar = &bars[wib][stage];
+    mbar_expect_tx(bar, kBulkG + kBulkW + (MODE == 2 ? 2 : 1) * kBulkBits);
+    bulk_g2s(st, p.in + static_cast<size_t>(w) * p.in_stride + kc + i0 + r0 * kRowElems - s, kBulkG, bar);
+    bulk_g2s(st + kBulkG, p.werr + ep * p.c_pad + i0 + r0 * kRowElems, kBulkW, bar);
+    bulk_g2s(st + kBulkG + kBulkW, p.pk_prev + ep * p.slot + (i0 >> 5) + 4 * r0, kBulkBits, bar);
+    if (MODE == 2)
+      bulk_g2s(st + kBulkG + kBulkW + kBulkBits,
+               p.res_prev + static_cast<size_t>(j) * p.slot + (i0 >> 5) + 4 * r0, kBulkBits, bar);
+  };
+
+  long long ptile = next_fast(gw);
+  int pr = 0;
+  auto advance = [&](long long& tile, int& r0) {
+    r0 += kBulkR;
+    if (r0 == kRowsPerTile) {
+      r0 = 0;
+      tile = next_fast(tile + nwarps);
+    }
+  };
+  for (int s = 0; s < kBulkStages; ++s) {
+    issue(s, ptile, pr);
+    advance(ptile, pr);
+  }
+
+  long long ctile = next_fast(gw);
+  int cr = 0;
+  uint32_t b = 0;
+  // per-tile consumer state
+  int s = 0, t = 0;
+  size_t ep = 0;
+  uint64_t i0 = 0, kc = 0;
+  float* we = nullptr;
+  uint32_t* pkc = nullptr;
+  uint32_t* rxw = nullptr;
+  float Sp = 0.f, pos_m = 0.f, neg_m = 0.f, A = 0.f, B = 0.f, IC = 0.f;
+  int w = 0;
+  double acc = 0.0;
+  float cm = 0.0f;
+  const bool stats = p.cmax != nullptr;
+  const uint32_t sh = 4 * (lane & 7);
+  const int wsub = lane >> 3;
+  while (ctile < total) {
+    const int stage = static_cast<int>(b % kBulkStages);
+    const uint32_t phase = (b / kBulkStages) & 1u;
+    if (cr == 0) {
+      w = static_cast<int>(ctile / per_w);
+      const long long rem = ctile - w * per_w;
+      const int j = static_cast<int>(rem / p.tpc);
+      t = static_cast<int>(rem - static_cast<long long>(j) * p.tpc);
+      i0 = static_cast<uint64_t>(t) * kTile;
+      kc = static_cast<uint64_t>(j) * p.c;
+      s = static_cast<int>(kc & 3u);
+      ep = static_cast<size_t>(w) * p.n + j;
+      we = p.werr + ep * p.c_pad + i0;
+      pkc = p.pk_cur + ep * p.slot + (i0 >> 5);
+      rxw = p.peer_rx ? p.peer_rx[j] + p.rx_off + (i0 >> 5) : nullptr;
+      Sp = slot_scale(p.pk_prev + ep * p.slot, p.W);
+      if (MODE == 2) {
+        const float S2 = slot_scale(p.res_prev + static_cast<size_t>(j) * p.slot, p.W);
+        pos_m = S2;
+        neg_m = S2 == 0.0f ? 0.0f : -S2;
+        const int l0 = __ldg(p.tile_layer + static_cast<size_t>(j) * p.tpc + t);
+        A = __ldg(p.A + l0);
+        B = __ldg(p.B + l0);
+        IC = __ldg(p.invc + l0);
+      }
+      acc = 0.0;
+      cm = 0.0f;
+    }
+    mbar_wait(&bars[wib][stage], phase);
+    const unsigned char* st = wsm + stage * kBulkStage;
+    const float* gsm = reinterpret_cast<const float*>(st) + s;
+    const float* wsm_rows = reinterpret_cast<const float*>(st + kBulkG);
+    const uint32_t* wbits = reinterpret_cast<const uint32_t*>(st + kBulkG + kBulkW);
+    const uint32_t* rbits = reinterpret_cast<const uint32_t*>(st + kBulkG + kBulkW + kBulkBits);
+#pragma unroll
+    for (int k = 0; k < kBulkR; ++k) {
+      const float4 g = lds_mis(gsm + k * kRowElems + 4 * lane, s);
+      const float4 raw = *reinterpret_cast<const float4*>(wsm_rows + k * kRowElems + 4 * lane);
+      const uint32_t wn = wbits[4 * k + wsub] >> sh;
+      const uint32_t rn = MODE == 2 ? rbits[4 * k + wsub] >> sh : 0u;
+      if (MODE == 2 && !(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w))) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (!isfinite(comp(g, q))) {
+            flag(p.err, kErrGrad,
+                 (static_cast<unsigned long long>(p.worker_base + w) << 40) |
+                     (kc + i0 + (cr + k) * kRowElems + 4 * lane + q));
+          }
+        }
+      }
+      uint32_t nib = 0;
+      float4 rawn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float v;
+        if (MODE == 0) {
+          v = comp(g, q);
+        } else {
+          const float mq = __fmul_rn((rn >> q) & 1u ? pos_m : neg_m, IC);  // fusion.cpp:143
+          v = __fadd_rn(__fmul_rn(A, mq), __fmul_rn(B, comp(g, q)));     // kernels.cpp:253
+        }
+        const float rec = (wn >> q) & 1u ? Sp : -Sp;
+        const float delta = __fsub_rn(comp(raw, q), rec);    // compression.cpp:194
+        const float corr = __fadd_rn(v, __fmul_rn(es, delta));  // :181
+        set_comp(rawn, q, __fadd_rn(v, delta));
+        nib |= static_cast<uint32_t>(corr >= 0.0f) << q;  // :50
+        acc += fabs(static_cast<double>(corr));           // :54
+        if (stats) {
+          const float ac = fabsf(corr);
+          cm = cm < ac ? ac : cm;
+        }
+      }
+      st4(we + (cr + k) * kRowElems + 4 * lane, rawn);
+      store_row_bits(pkc, cr + k, lane, nib);
+    }
+    if (cr + kBulkR == kRowsPerTile) {
+      const double tot = warp_bfly_sum(acc);
+      if (lane == 0) p.partials[ep * p.tpc + t] = tot;
+      if (stats) {
+        const float m = warp_max(cm);
+        if (lane == 0) p.cmax[ep * p.tpc + t] = m;
+      }
+      if (rxw) push_tile(pkc, rxw, lane);  // fused alltoall
+    }
+    __syncwarp();  // every lane is done with this stage before it is refilled
+    issue(stage, ptile, pr);
+    advance(ptile, pr);
+    advance(ctile, cr);
+    ++b;
+  }
+  if (p.peer_rx) warp_fence_system(lane);
 }
 
 // Scale of each endpoint: S = (float)(sum|corrected| / c) (compression.cpp:54-55),
@@ -1363,7 +1610,38 @@ int grid_for_elems(uint64_t n) {
 
 }  // namespace
 
+template <int MODE>
+int launch_k1_bulk(const K1Params& p, cudaStream_t s) {
+  static thread_local int grid = 0;
+  if (grid == 0) {
+    cudaFuncSetAttribute(k1_bulk<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_bulk<MODE>, kBulkWarps * 32, kBulkSmem);
+    grid = sms * (occ > 0 ? occ : 1);
+  }
+  k1_bulk<MODE><<<grid, kBulkWarps * 32, kBulkSmem, s>>>(p);
+  return 1;
+}
+
 int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
+  if (mode != 1 && (mode == 0 || p.tile_layer)) {
+    // Fast tiles through the bulk-copy pipeline, then the rest (boundary
+    // tiles) through the general kernel.
+    int k = mode == 0 ? launch_k1_bulk<0>(p, s) : launch_k1_bulk<2>(p, s);
+    K1Params q = p;
+    q.skip_fast = 1;
+    const bool al = (p.c & 3u) == 0;
+    if (mode == 0) {
+      if (al) k1_worker_compress<0, true><<<resident(k1_worker_compress<0, true>, grid), kBlock, 0, s>>>(q);
+      else k1_worker_compress<0, false><<<resident(k1_worker_compress<0, false>, grid), kBlock, 0, s>>>(q);
+    } else {
+      if (al) k1_worker_compress<2, true><<<resident(k1_worker_compress<2, true>, grid), kBlock, 0, s>>>(q);
+      else k1_worker_compress<2, false><<<resident(k1_worker_compress<2, false>, grid), kBlock, 0, s>>>(q);
+    }
+    return k + 1;
+  }
 #define BL_K1(M, A) k1_worker_compress<M, A><<<resident(k1_worker_compress<M, A>, grid), kBlock, 0, s>>>(p)
   const bool al = (p.c & 3u) == 0;  // every chunk start 16-byte aligned
   switch (mode) {

@@ -61,6 +61,8 @@ struct K1Params {
   // also stored into rank j's receive slot peer_rx[j] + rx_off.
   uint32_t* const* peer_rx;   // [n] peer receive-buffer bases (nullptr: no fused exchange)
   uint64_t rx_off;            // word offset of this rank's slot in the current parity
+  const int* tile_layer;      // mode 2: [n][tpc] layer of a single-layer full tile, else -1
+  int skip_fast;              // general kernel: leave fast tiles to the bulk kernel
 };
 
 // K3: server reduction of chunk(s) owned locally.

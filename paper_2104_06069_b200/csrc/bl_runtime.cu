@@ -567,6 +567,7 @@ void bl_optimizer::compressed_step(double lr) {
     p.A = A;
     p.B = B;
     p.invc = invc;
+    p.tile_layer = k1_tile_layer;
     cl->compressed(&p, mode, 1.0f, es);
   }
 
@@ -1166,6 +1167,21 @@ bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_
       o->es = dalloc<float>(1);
       o->counter = reinterpret_cast<unsigned int*>(dalloc<float>(1));
       o->tile_sums = dalloc<double>(4 * static_cast<size_t>(o->tiles));
+      {  // K1 tiles (chunk-relative) that are full and inside one layer
+        std::vector<int> k1l(static_cast<size_t>(cl->n) * cl->tpc, -1);
+        for (int j = 0; j < cl->n; ++j) {
+          for (int t = 0; t < cl->tpc; ++t) {
+            const uint64_t i0 = static_cast<uint64_t>(t) * kTile, k0 = static_cast<uint64_t>(j) * cl->c + i0;
+            if (i0 + kTile > cl->c || k0 + kTile > o->d) continue;
+            const auto it = std::upper_bound(o->off.begin(), o->off.end(), k0);
+            const int l = static_cast<int>(it - o->off.begin()) - 1;
+            if (k0 + kTile - 1 < o->off[l + 1]) k1l[static_cast<size_t>(j) * cl->tpc + t] = l;
+          }
+        }
+        o->k1_tile_layer = reinterpret_cast<int*>(dalloc<float>(k1l.size()));
+        cuda_check(cudaMemcpy(o->k1_tile_layer, k1l.data(), k1l.size() * 4, cudaMemcpyHostToDevice),
+                   "k1 tiles");
+      }
       o->tile_max = dalloc<float>(static_cast<size_t>(o->tiles));
       std::vector<double> ones(L, 1.0);
       std::vector<float> onesf(L, 1.0f);
@@ -1188,7 +1204,8 @@ void bl_optimizer_destroy(bl_optimizer* o) {
   cudaStreamSynchronize(o->cl->stream);
   void* bufs[] = {o->off_dev, o->tile_layer, o->layer_tile_start, o->x, o->m, o->v, o->vf,
                   o->mprev, o->c_avg, o->r_prev, o->coeff, o->mag, o->A, o->B, o->invc, o->coef_x,
-                  o->trace, o->cmean, o->es, o->counter, o->tile_sums, o->tile_max};
+                  o->trace, o->cmean, o->es, o->counter, o->tile_sums, o->tile_max,
+                  o->k1_tile_layer};
   for (void* p : bufs)
     if (p) cudaFree(p);
   delete o;

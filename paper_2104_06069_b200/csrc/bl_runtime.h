@@ -149,6 +149,7 @@ struct bl_optimizer {
   unsigned int* counter = nullptr;
   double* tile_sums = nullptr;  // [tiles][4]
   float* tile_max = nullptr;    // [tiles]
+  int* k1_tile_layer = nullptr;  // [n][tpc]: layer of a full single-layer K1 tile, else -1
   bool frozen = false, has_vf = false, has_mprev = false;
   bool m_valid = true;          // m buffer holds m (else: decompressed result * invc)
   bool mprev_separate = false;  // m_prev poked by the caller
