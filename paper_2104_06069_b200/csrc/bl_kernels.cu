@@ -12,6 +12,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 #include <unordered_map>
 
 #include "bl_kernels.cuh"
@@ -286,10 +288,15 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const long long per_w = static_cast<long long>(p.n) * p.tpc;
-  const long long total = per_w * p.nw;
+  const long long total = p.slow_list ? static_cast<long long>(p.n_slow) * p.nw : per_w * p.nw;
   const float es = p.es_dev ? __ldg(p.es_dev) : p.es_host;
 
-  for (long long tile = gw; tile < total; tile += nwarps) {
+  for (long long it = gw; it < total; it += nwarps) {
+    long long tile = it;
+    if (p.slow_list) {  // iterate only the listed boundary tiles of every worker
+      const long long wl = it / p.n_slow;
+      tile = wl * per_w + __ldg(p.slow_list + (it - wl * p.n_slow));
+    }
     const int w = static_cast<int>(tile / per_w);
     const long long rem = tile - w * per_w;
     const int j = static_cast<int>(rem / p.tpc);
@@ -515,12 +522,14 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
 // ---------------------------------------------------------------------------
 constexpr int kBulkWarps = 4;
 constexpr int kBulkStages = 3;
-constexpr int kBulkR = 4;
-constexpr int kBulkG = (kBulkR * kRowElems + 4) * 4;  // 2064 B
-constexpr int kBulkW = kBulkR * kRowElems * 4;        // 2048 B
-constexpr int kBulkBits = kBulkR * 4 * 4;             // 64 B
-constexpr int kBulkStage = kBulkG + kBulkW + 2 * kBulkBits;
-constexpr int kBulkSmem = kBulkWarps * kBulkStages * kBulkStage;
+template <int R>
+struct BulkGeom {
+  static constexpr int G = (R * kRowElems + 4) * 4;  // g rows + alignment slack
+  static constexpr int Wb = R * kRowElems * 4;       // werr rows
+  static constexpr int Bits = R * 4 * 4;             // packet words of the rows
+  static constexpr int Stage = G + Wb + 2 * Bits;
+  static constexpr int Smem = kBulkWarps * kBulkStages * Stage;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -572,8 +581,10 @@ __device__ __forceinline__ int k1_fast_layer(const K1Params& p, int j, int t) {
   return __ldg(p.tile_layer + static_cast<size_t>(j) * p.tpc + t);
 }
 
-template <int MODE>
+template <int MODE, int kBulkR>
 __global__ void __launch_bounds__(kBulkWarps * 32) k1_bulk(const K1Params p) {
+  using Geo = BulkGeom<kBulkR>;
+  constexpr int kBulkG = Geo::G, kBulkW = Geo::Wb, kBulkBits = Geo::Bits, kBulkStage = Geo::Stage;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) unsigned long long bars[kBulkWarps][kBulkStages];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1610,28 +1621,51 @@ int grid_for_elems(uint64_t n) {
 
 }  // namespace
 
-template <int MODE>
+template <int MODE, int R>
 int launch_k1_bulk(const K1Params& p, cudaStream_t s) {
   static thread_local int grid = 0;
+  constexpr int smem = BulkGeom<R>::Smem;
   if (grid == 0) {
-    cudaFuncSetAttribute(k1_bulk<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
+    cudaFuncSetAttribute(k1_bulk<MODE, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_bulk<MODE>, kBulkWarps * 32, kBulkSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_bulk<MODE, R>, kBulkWarps * 32, smem);
     grid = sms * (occ > 0 ? occ : 1);
   }
-  k1_bulk<MODE><<<grid, kBulkWarps * 32, kBulkSmem, s>>>(p);
+  k1_bulk<MODE, R><<<grid, kBulkWarps * 32, smem, s>>>(p);
   return 1;
 }
 
+// Rows per bulk stage (BL_K1_BULK_R=4|8, default 8) and whether aligned
+// chunks also take the bulk path (BL_K1_BULK=all) — tuning knobs.
+static int bulk_rows() {
+  static const int r = [] {
+    const char* e = std::getenv("BL_K1_BULK_R");
+    return e && std::atoi(e) == 4 ? 4 : 8;
+  }();
+  return r;
+}
+static bool bulk_all() {
+  static const bool a = [] {
+    const char* e = std::getenv("BL_K1_BULK");
+    return e && std::string(e) == "all";
+  }();
+  return a;
+}
+
 int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
-  if (mode != 1 && (mode == 0 || p.tile_layer)) {
-    // Fast tiles through the bulk-copy pipeline, then the rest (boundary
-    // tiles) through the general kernel.
-    int k = mode == 0 ? launch_k1_bulk<0>(p, s) : launch_k1_bulk<2>(p, s);
+  const bool misaligned = (p.c & 3u) != 0;
+  if (mode != 1 && (mode == 0 || p.tile_layer) && (misaligned || bulk_all())) {
+    // Misaligned chunks: fast tiles through the bulk-copy pipeline (g staged
+    // with alignment slack), then the boundary tiles through the general
+    // kernel.  Aligned chunks stay on the register path, which measures faster.
+    int k;
+    if (bulk_rows() == 4) k = mode == 0 ? launch_k1_bulk<0, 4>(p, s) : launch_k1_bulk<2, 4>(p, s);
+    else k = mode == 0 ? launch_k1_bulk<0, 8>(p, s) : launch_k1_bulk<2, 8>(p, s);
     K1Params q = p;
     q.skip_fast = 1;
+    if (q.slow_list && q.n_slow == 0) return k;  // no boundary tiles
     const bool al = (p.c & 3u) == 0;
     if (mode == 0) {
       if (al) k1_worker_compress<0, true><<<resident(k1_worker_compress<0, true>, grid), kBlock, 0, s>>>(q);
@@ -1642,7 +1676,11 @@ int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
     }
     return k + 1;
   }
-#define BL_K1(M, A) k1_worker_compress<M, A><<<resident(k1_worker_compress<M, A>, grid), kBlock, 0, s>>>(p)
+  K1Params full = p;  // register path: every tile, the slow list does not apply
+  full.slow_list = nullptr;
+  full.n_slow = 0;
+  full.skip_fast = 0;
+#define BL_K1(M, A) k1_worker_compress<M, A><<<resident(k1_worker_compress<M, A>, grid), kBlock, 0, s>>>(full)
   const bool al = (p.c & 3u) == 0;  // every chunk start 16-byte aligned
   switch (mode) {
     case 0: if (al) BL_K1(0, true); else BL_K1(0, false); break;

@@ -63,6 +63,8 @@ struct K1Params {
   uint64_t rx_off;            // word offset of this rank's slot in the current parity
   const int* tile_layer;      // mode 2: [n][tpc] layer of a single-layer full tile, else -1
   int skip_fast;              // general kernel: leave fast tiles to the bulk kernel
+  const int* slow_list;       // general kernel after k1_bulk: the non-fast (j*tpc+t) tiles
+  int n_slow;
 };
 
 // K3: server reduction of chunk(s) owned locally.

@@ -144,6 +144,10 @@ void bl_cluster::copy_inputs(const float* const* inputs, int n_inputs, uint64_t 
 
 void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, const float* es_dev) {
   K1Params p = ovr ? *ovr : K1Params{};
+  if (!ovr) {
+    p.slow_list = k1_slow;
+    p.n_slow = k1_n_slow;
+  }
   p.n = n;
   p.nw = nw;
   p.tpc = tpc;
@@ -568,6 +572,8 @@ void bl_optimizer::compressed_step(double lr) {
     p.B = B;
     p.invc = invc;
     p.tile_layer = k1_tile_layer;
+    p.slow_list = k1_slow;
+    p.n_slow = k1_n_slow;
     cl->compressed(&p, mode, 1.0f, es);
   }
 
@@ -838,6 +844,20 @@ bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
         c->stat_out = dalloc<double>(2);
       }
       c->stats.assign(2 * n, bl_endpoint_stats{});
+      {  // API-mode K1 boundary tiles: not full, or reaching into the padding
+        std::vector<int> slow;
+        for (int j = 0; j < c->n; ++j)
+          for (int t = 0; t < c->tpc; ++t) {
+            const uint64_t i0 = static_cast<uint64_t>(t) * kTile;
+            if (i0 + kTile > c->c || static_cast<uint64_t>(j) * c->c + i0 + kTile > c->dim)
+              slow.push_back(j * c->tpc + t);
+          }
+        c->k1_n_slow = static_cast<int>(slow.size());
+        c->k1_slow = reinterpret_cast<int*>(dalloc<float>(slow.size()));
+        if (!slow.empty())
+          cuda_check(cudaMemcpy(c->k1_slow, slow.data(), slow.size() * 4, cudaMemcpyHostToDevice),
+                     "k1 slow tiles");
+      }
       if (c->mode == BL_MODE_NCCL) {
         c->rpk = dalloc<uint32_t>(n * c->slot);
         c->lrecv = dalloc<float>(n * c->c_pad + kSlack);
@@ -867,7 +887,7 @@ void bl_cluster_destroy(bl_cluster* c) {
                   c->serr,      c->res_base,   c->wpart,           c->spart,     c->wcmax,
                   c->scmax,     c->out,        c->lrecv,           c->err,       c->stat_part,
                   c->stat_max,  c->stat_out,   c->rx,              c->flags,     c->d_peer_rx,
-                  c->d_peer_res, c->d_peer_flags};
+                  c->d_peer_res, c->d_peer_flags, c->k1_slow};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& e : c->pending) {
@@ -1181,6 +1201,14 @@ bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_
         o->k1_tile_layer = reinterpret_cast<int*>(dalloc<float>(k1l.size()));
         cuda_check(cudaMemcpy(o->k1_tile_layer, k1l.data(), k1l.size() * 4, cudaMemcpyHostToDevice),
                    "k1 tiles");
+        std::vector<int> slow;
+        for (size_t k = 0; k < k1l.size(); ++k)
+          if (k1l[k] < 0) slow.push_back(static_cast<int>(k));
+        o->k1_n_slow = static_cast<int>(slow.size());
+        o->k1_slow = reinterpret_cast<int*>(dalloc<float>(slow.size()));
+        if (!slow.empty())
+          cuda_check(cudaMemcpy(o->k1_slow, slow.data(), slow.size() * 4, cudaMemcpyHostToDevice),
+                     "k1 slow tiles");
       }
       o->tile_max = dalloc<float>(static_cast<size_t>(o->tiles));
       std::vector<double> ones(L, 1.0);
@@ -1205,7 +1233,7 @@ void bl_optimizer_destroy(bl_optimizer* o) {
   void* bufs[] = {o->off_dev, o->tile_layer, o->layer_tile_start, o->x, o->m, o->v, o->vf,
                   o->mprev, o->c_avg, o->r_prev, o->coeff, o->mag, o->A, o->B, o->invc, o->coef_x,
                   o->trace, o->cmean, o->es, o->counter, o->tile_sums, o->tile_max,
-                  o->k1_tile_layer};
+                  o->k1_tile_layer, o->k1_slow};
   for (void* p : bufs)
     if (p) cudaFree(p);
   delete o;

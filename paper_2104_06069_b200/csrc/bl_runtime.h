@@ -90,6 +90,9 @@ struct bl_cluster {
   std::vector<void*> ipc_opened;
   void setup_p2p(bool required);
 
+  int* k1_slow = nullptr;       // API-mode K1 tiles that are not full/inside the data
+  int k1_n_slow = 0;
+
   uint64_t calls = 0;           // compressed collectives run (ping-pong index)
   bool last_identity = false;
   bl_volume_ledger ledger{};
@@ -150,6 +153,8 @@ struct bl_optimizer {
   double* tile_sums = nullptr;  // [tiles][4]
   float* tile_max = nullptr;    // [tiles]
   int* k1_tile_layer = nullptr;  // [n][tpc]: layer of a full single-layer K1 tile, else -1
+  int* k1_slow = nullptr;        // the remaining (j*tpc+t) tiles
+  int k1_n_slow = 0;
   bool frozen = false, has_vf = false, has_mprev = false;
   bool m_valid = true;          // m buffer holds m (else: decompressed result * invc)
   bool mprev_separate = false;  // m_prev poked by the caller
