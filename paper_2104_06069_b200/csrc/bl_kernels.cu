@@ -194,6 +194,27 @@ __device__ __forceinline__ void push_tile(const uint32_t* local, uint32_t* remot
   reinterpret_cast<uint4*>(remote)[lane] = v;
 }
 
+// Packet words of a tile are staged in a per-warp shared buffer (128 words)
+// and leave it once per tile as one 16-byte store per lane — locally and, for
+// the fused exchange, into peer HBM — instead of 4-byte stores per row.
+__device__ __forceinline__ void stage_row_bits(uint32_t* sw, int r, int lane, uint32_t nib) {
+  uint32_t v = nib << (4 * (lane & 7));
+  v |= __shfl_xor_sync(FULL, v, 1);
+  v |= __shfl_xor_sync(FULL, v, 2);
+  v |= __shfl_xor_sync(FULL, v, 4);
+  if ((lane & 7) == 0) sw[4 * r + (lane >> 3)] = v;
+}
+__device__ __forceinline__ void clear_tile_words(uint32_t* sw, int lane) {
+  reinterpret_cast<uint4*>(sw)[lane] = make_uint4(0u, 0u, 0u, 0u);
+  __syncwarp();
+}
+__device__ __forceinline__ uint4 tile_words(const uint32_t* sw, int lane) {
+  __syncwarp();
+  const uint4 v = reinterpret_cast<const uint4*>(sw)[lane];
+  __syncwarp();  // the buffer may be refilled after this
+  return v;
+}
+
 // Make this warp's remote (peer-memory) stores visible system-wide before the
 // stream's next kernel raises the peer flag: warp barrier, then one fence.
 __device__ __forceinline__ void warp_fence_system(int lane) {
@@ -284,6 +305,8 @@ __device__ __forceinline__ void wait_peers(const unsigned long long* flags, int 
 // ---------------------------------------------------------------------------
 template <int MODE, bool ALIGNED>
 __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p) {
+  __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
+  uint32_t* sw = s_words[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -398,16 +421,18 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
             }
           }
           st4(we + (r0 + k) * kRowElems + 4 * lane, rawn);
-          store_row_bits(pkc, r0 + k, lane, nib);
+          stage_row_bits(sw, r0 + k, lane, nib);
         }
       }
+      const uint4 wv = tile_words(sw, lane);
+      reinterpret_cast<uint4*>(pkc)[lane] = wv;
+      if (rxw) reinterpret_cast<uint4*>(rxw)[lane] = wv;  // fused alltoall
       acc = warp_bfly_sum(acc);
       if (lane == 0) p.partials[ep * p.tpc + t] = acc;
       if (stats) {
         cm = warp_max(cm);
         if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
       }
-      if (rxw) push_tile(pkc, rxw, lane);  // fused alltoall
       continue;
     }
 
@@ -415,6 +440,7 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
     int lcache = -1;
     if (MODE != 0) l = find_layer(p.off, p.L, kc + i0);
 
+    clear_tile_words(sw, lane);  // rows past the chunk end keep zero bits
     double acc = 0.0;
     float cm = 0.0f;
     for (int r = 0; r < kRowsPerTile; ++r) {
@@ -498,7 +524,12 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
         }
       }
       st4(we + r * kRowElems + 4 * lane, rawn);
-      store_row_bits(pkc, r, lane, nib);
+      stage_row_bits(sw, r, lane, nib);
+    }
+    {
+      const uint4 wv = tile_words(sw, lane);
+      reinterpret_cast<uint4*>(pkc)[lane] = wv;
+      if (rxw) reinterpret_cast<uint4*>(rxw)[lane] = wv;
     }
     acc = warp_bfly_sum(acc);
     if (lane == 0) p.partials[ep * p.tpc + t] = acc;
@@ -506,7 +537,6 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
       cm = warp_max(cm);
       if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
     }
-    if (rxw) push_tile(pkc, rxw, lane);
   }
   if (p.peer_rx) warp_fence_system(threadIdx.x & 31);  // remote words before the finalize signal
 }
@@ -582,12 +612,14 @@ __device__ __forceinline__ int k1_fast_layer(const K1Params& p, int j, int t) {
 }
 
 template <int MODE, int kBulkR>
-__global__ void __launch_bounds__(kBulkWarps * 32) k1_bulk(const K1Params p) {
+__global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) {
   using Geo = BulkGeom<kBulkR>;
   constexpr int kBulkG = Geo::G, kBulkW = Geo::Wb, kBulkBits = Geo::Bits, kBulkStage = Geo::Stage;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) unsigned long long bars[kBulkWarps][kBulkStages];
+  __shared__ __align__(16) uint32_t s_words[kBulkWarps][128];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint32_t* sw = s_words[wib];
   unsigned char* wsm = sm + wib * kBulkStages * kBulkStage;
   const long long gw = static_cast<long long>(blockIdx.x) * kBulkWarps + wib;
   const long long nwarps = static_cast<long long>(gridDim.x) * kBulkWarps;
@@ -735,20 +767,22 @@ __global__ void __launch_bounds__(kBulkWarps * 32) k1_bulk(const K1Params p) {
         }
       }
       st4(we + (cr + k) * kRowElems + 4 * lane, rawn);
-      store_row_bits(pkc, cr + k, lane, nib);
+      stage_row_bits(sw, cr + k, lane, nib);
     }
+    __syncwarp();  // every lane is done with this stage before it is refilled
+    issue(stage, ptile, pr);
+    advance(ptile, pr);
     if (cr + kBulkR == kRowsPerTile) {
+      const uint4 wv = tile_words(sw, lane);
+      reinterpret_cast<uint4*>(pkc)[lane] = wv;
+      if (rxw) reinterpret_cast<uint4*>(rxw)[lane] = wv;  // fused alltoall
       const double tot = warp_bfly_sum(acc);
       if (lane == 0) p.partials[ep * p.tpc + t] = tot;
       if (stats) {
         const float m = warp_max(cm);
         if (lane == 0) p.cmax[ep * p.tpc + t] = m;
       }
-      if (rxw) push_tile(pkc, rxw, lane);  // fused alltoall
     }
-    __syncwarp();  // every lane is done with this stage before it is refilled
-    issue(stage, ptile, pr);
-    advance(ptile, pr);
     advance(ctile, cr);
     ++b;
   }
@@ -784,12 +818,15 @@ __global__ void __launch_bounds__(1024) k_finalize_scales(const FinalizeParams p
 // ---------------------------------------------------------------------------
 // Allgather fused into K3: the row's 4 server words (just written to the local
 // result slot by the same warp) are copied into every peer's result slot.
-__device__ __forceinline__ void push_all(const K3Params& p, uint32_t* const* peers,
-                                         const uint32_t* rc, uint64_t i0, int lane) {
-  __syncwarp();
-  const uint4 v = __ldcg(reinterpret_cast<const uint4*>(rc) + lane);
-  for (int q = 0; q < p.n; ++q) {
-    if (q != p.rank) reinterpret_cast<uint4*>(peers[q] + p.res_off + (i0 >> 5))[lane] = v;
+__device__ __forceinline__ void flush_server_words(const K3Params& p, uint32_t* const* peers,
+                                                   const uint32_t* sw, uint32_t* rc, uint64_t i0,
+                                                   int lane) {
+  const uint4 v = tile_words(sw, lane);
+  reinterpret_cast<uint4*>(rc)[lane] = v;
+  if (p.peer_res) {
+    for (int q = 0; q < p.n; ++q) {
+      if (q != p.rank) reinterpret_cast<uint4*>(peers[q] + p.res_off + (i0 >> 5))[lane] = v;
+    }
   }
 }
 
@@ -797,6 +834,8 @@ template <int NT>
 __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
   __shared__ float s_scale[kWarpsPerBlock][64];
   __shared__ uint32_t* s_peer[64];
+  __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
+  uint32_t* sw = s_words[threadIdx.x >> 5];
   const int n = NT > 0 ? NT : p.n;
   if (p.peer_res) {
     for (int q = threadIdx.x; q < p.n; q += blockDim.x) s_peer[q] = p.peer_res[q];
@@ -878,7 +917,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
             }
           }
           st4(se + (r0 + k) * kRowElems + 4 * lane, rawn);
-          store_row_bits(rc, r0 + k, lane, nib);
+          stage_row_bits(sw, r0 + k, lane, nib);
         }
       }
       acc = warp_bfly_sum(acc);
@@ -887,10 +926,11 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
         cm = warp_max(cm);
         if (lane == 0) p.cmax[static_cast<size_t>(sv) * p.tpc + t] = cm;
       }
-      if (p.peer_res) push_all(p, s_peer, rc, i0, lane);  // fused allgather
+      flush_server_words(p, s_peer, sw, rc, i0, lane);  // local + fused allgather
       continue;
     }
 
+    clear_tile_words(sw, lane);
     double acc = 0.0;
     float cm = 0.0f;
     for (int r = 0; r < kRowsPerTile; ++r) {
@@ -933,7 +973,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
         }
       }
       st4(se + r * kRowElems + 4 * lane, rawn);
-      store_row_bits(rc, r, lane, nib);
+      stage_row_bits(sw, r, lane, nib);
     }
     acc = warp_bfly_sum(acc);
     if (lane == 0) p.partials[static_cast<size_t>(sv) * p.tpc + t] = acc;
@@ -941,7 +981,7 @@ __global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
       cm = warp_max(cm);
       if (lane == 0) p.cmax[static_cast<size_t>(sv) * p.tpc + t] = cm;
     }
-    if (p.peer_res) push_all(p, s_peer, rc, i0, lane);
+    flush_server_words(p, s_peer, sw, rc, i0, lane);
   }
   if (p.peer_res) warp_fence_system(lane);  // remote server words before the finalize signal
 }
