@@ -831,7 +831,7 @@ __device__ __forceinline__ void flush_server_words(const K3Params& p, uint32_t* 
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kBlock) k3_server_reduce(const K3Params p) {
+__global__ void __launch_bounds__(kBlock, (NT > 0 && NT <= 2) ? 4 : 2) k3_server_reduce(const K3Params p) {
   __shared__ float s_scale[kWarpsPerBlock][64];
   __shared__ uint32_t* s_peer[64];
   __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
@@ -1693,10 +1693,17 @@ static bool bulk_all() {
   }();
   return a;
 }
+static bool bulk_none() {
+  static const bool a = [] {
+    const char* e = std::getenv("BL_K1_BULK");
+    return e && std::string(e) == "none";
+  }();
+  return a;
+}
 
 int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
   const bool misaligned = (p.c & 3u) != 0;
-  if (mode != 1 && (mode == 0 || p.tile_layer) && (misaligned || bulk_all())) {
+  if (mode != 1 && (mode == 0 || p.tile_layer) && (misaligned || bulk_all()) && !bulk_none()) {
     // Misaligned chunks: fast tiles through the bulk-copy pipeline (g staged
     // with alignment slack), then the boundary tiles through the general
     // kernel.  Aligned chunks stay on the register path, which measures faster.
