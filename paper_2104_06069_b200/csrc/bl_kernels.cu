@@ -1701,9 +1701,27 @@ static bool bulk_none() {
   return a;
 }
 
-int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
+bool k1_uses_bulk(const K1Params& p, int mode) {
   const bool misaligned = (p.c & 3u) != 0;
-  if (mode != 1 && (mode == 0 || p.tile_layer) && (misaligned || bulk_all()) && !bulk_none()) {
+  return mode != 1 && (mode == 0 || p.tile_layer) && (misaligned || bulk_all()) && !bulk_none();
+}
+
+int launch_k1_phase(const K1Params& p, int mode, int phase, cudaStream_t s) {
+  if (phase == 0) {
+    if (bulk_rows() == 4) return mode == 0 ? launch_k1_bulk<0, 4>(p, s) : launch_k1_bulk<2, 4>(p, s);
+    return mode == 0 ? launch_k1_bulk<0, 8>(p, s) : launch_k1_bulk<2, 8>(p, s);
+  }
+  K1Params q = p;
+  q.skip_fast = 1;
+  if (q.slow_list && q.n_slow == 0) return 0;
+  const int g = resident(k1_worker_compress<2, false>, 148 * 16);
+  if (mode == 0) k1_worker_compress<0, false><<<g, kBlock, 0, s>>>(q);
+  else k1_worker_compress<2, false><<<g, kBlock, 0, s>>>(q);
+  return 1;
+}
+
+int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
+  if (k1_uses_bulk(p, mode)) {
     // Misaligned chunks: fast tiles through the bulk-copy pipeline (g staged
     // with alignment slack), then the boundary tiles through the general
     // kernel.  Aligned chunks stay on the register path, which measures faster.

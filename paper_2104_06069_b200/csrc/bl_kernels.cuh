@@ -213,6 +213,10 @@ struct W2Params {
 
 // Host launchers (bl_kernels.cu).  Each returns the number of kernels launched.
 int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s);
+// The two launches of the bulk-copy K1: phase 0 = fast tiles (k1_bulk),
+// phase 1 = boundary tiles (general kernel over the slow list).
+bool k1_uses_bulk(const K1Params& p, int mode);
+int launch_k1_phase(const K1Params& p, int mode, int phase, cudaStream_t s);
 int launch_finalize(const FinalizeParams& p, int count, cudaStream_t s);
 int launch_k3(const K3Params& p, int grid, cudaStream_t s);
 int launch_k5(const K5Params& p, int grid, cudaStream_t s);

@@ -24,7 +24,7 @@ const char* const kClassNames[KC_COUNT] = {
     "layer_epilogue",     "k6_update_b",     "w1_warmup_a",      "warmup_epilogue",
     "w2_warmup_b",        "average",         "decompress",       "materialize",
     "endpoint_stats",     "nccl_alltoall",   "nccl_allgather",   "h2d_copy",
-    "d2h_copy"};
+    "d2h_copy",           "k1_boundary_tiles"};
 
 void fail(bl_status st, const std::string& msg) { throw Error{st, msg}; }
 
@@ -175,8 +175,15 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
     p.rx_off = my_slot;
   }
   cudaEvent_t a;
-  begin(KC_K1, &a);
-  end(KC_K1, a, launch_k1(p, k1_mode, grid(static_cast<long long>(nw) * n * tpc), stream));
+  if (k1_uses_bulk(p, k1_mode)) {  // bulk fast tiles, then the boundary tiles
+    begin(KC_K1, &a);
+    end(KC_K1, a, launch_k1_phase(p, k1_mode, 0, stream));
+    begin(KC_K1B, &a);
+    end(KC_K1B, a, launch_k1_phase(p, k1_mode, 1, stream));
+  } else {
+    begin(KC_K1, &a);
+    end(KC_K1, a, launch_k1(p, k1_mode, grid(static_cast<long long>(nw) * n * tpc), stream));
+  }
 
   FinalizeParams f{wpart, tpc, c, wpk[cur()], slot, W, err, p.worker_base * n};
   if (p2p) {

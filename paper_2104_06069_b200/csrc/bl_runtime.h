@@ -43,7 +43,7 @@ class DeviceGuard {
 // Kernel classes for launch counting and optional CUDA-event timing.
 enum KClass : int {
   KC_K1 = 0, KC_FIN, KC_K3, KC_K5, KC_EPI, KC_K6, KC_W1, KC_WEPI, KC_W2, KC_AVG,
-  KC_DEC, KC_MAT, KC_STATS, KC_A2A, KC_AG, KC_H2D, KC_D2H, KC_COUNT
+  KC_DEC, KC_MAT, KC_STATS, KC_A2A, KC_AG, KC_H2D, KC_D2H, KC_K1B, KC_COUNT
 };
 extern const char* const kClassNames[KC_COUNT];
 
