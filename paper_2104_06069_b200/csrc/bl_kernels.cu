@@ -185,15 +185,6 @@ __device__ __forceinline__ uint32_t store_row_bits(uint32_t* words, int r, int l
   return v;
 }
 
-// Copy a finished tile's 128 packet words (512 B, just written locally by
-// this warp) to a peer slot with one 16-byte store per lane: whole NVLink
-// packets instead of scattered 4-byte writes.
-__device__ __forceinline__ void push_tile(const uint32_t* local, uint32_t* remote, int lane) {
-  __syncwarp();
-  const uint4 v = __ldcg(reinterpret_cast<const uint4*>(local) + lane);
-  reinterpret_cast<uint4*>(remote)[lane] = v;
-}
-
 // Packet words of a tile are staged in a per-warp shared buffer (128 words)
 // and leave it once per tile as one 16-byte store per lane — locally and, for
 // the fused exchange, into peer HBM — instead of 4-byte stores per row.
@@ -303,6 +294,231 @@ __device__ __forceinline__ void wait_peers(const unsigned long long* flags, int 
 // materialised from the previous packet when read.  Identical arithmetic,
 // one pass: 12 B/elem read + 4 B/elem written + 1 bit.
 // ---------------------------------------------------------------------------
+// One K1 tile (general path: any alignment, layer boundaries, padding, partial
+// tiles).  The per-warp word buffer `sw` stages the tile's packet words.
+template <int MODE, bool ALIGNED>
+__device__ __forceinline__ void k1_tile(const K1Params& p, long long tile, int lane, uint32_t* sw,
+                                        float es) {
+  const long long per_w = static_cast<long long>(p.n) * p.tpc;
+  const int w = static_cast<int>(tile / per_w);
+  const long long rem = tile - w * per_w;
+  const int j = static_cast<int>(rem / p.tpc);
+  const int t = static_cast<int>(rem - static_cast<long long>(j) * p.tpc);
+  const uint64_t i0 = static_cast<uint64_t>(t) * kTile;  // chunk-relative
+  const uint64_t kc = static_cast<uint64_t>(j) * p.c;    // global chunk start
+  const int s = ALIGNED ? 0 : static_cast<int>(kc & 3u);  // ALIGNED: c % 4 == 0
+  const size_t ep = static_cast<size_t>(w) * p.n + j;    // endpoint (worker, chunk)
+  const float* gin = p.in + static_cast<size_t>(w) * p.in_stride + kc + i0;
+  float* we = p.werr + ep * p.c_pad + i0;
+  const uint32_t* pkp = p.pk_prev + ep * p.slot;
+  uint32_t* pkc = p.pk_cur + ep * p.slot + (i0 >> 5);
+  uint32_t* rxw = p.peer_rx ? p.peer_rx[j] + p.rx_off + (i0 >> 5) : nullptr;
+  const float Sp = slot_scale(pkp, p.W);
+  pkp += i0 >> 5;
+
+  float pos_m = 0.f, neg_m = 0.f;
+  const uint32_t* rp = nullptr;
+  if (MODE == 2) {
+    const uint32_t* rs = p.res_prev + static_cast<size_t>(j) * p.slot;
+    const float S2 = slot_scale(rs, p.W);
+    pos_m = S2;
+    neg_m = S2 == 0.0f ? 0.0f : -S2;
+    rp = rs + (i0 >> 5);
+  }
+  float A = 0.f, B = 0.f, IC = 0.f;
+
+  // Fast path: the whole tile lies inside the chunk, inside the real
+  // (unpadded) data and inside one layer.  Rows are processed 4 at a time
+  // with all loads issued first; same per-element arithmetic and the same
+  // accumulation order as the general path below.
+  bool fast = MODE != 1 && i0 + kTile <= p.c && kc + i0 + kTile <= p.d;
+  if (fast && MODE == 2) {
+    int l0;
+    if (p.tile_layer) {
+      l0 = __ldg(p.tile_layer + static_cast<size_t>(j) * p.tpc + t);
+      fast = l0 >= 0;
+    } else {
+      l0 = find_layer(p.off, p.L, kc + i0);
+      fast = l0 < p.L && kc + i0 + (kTile - 1) < __ldg(p.off + l0 + 1);
+    }
+    if (fast) {
+      A = __ldg(p.A + l0);
+      B = __ldg(p.B + l0);
+      IC = __ldg(p.invc + l0);
+    }
+  }
+  if (fast && p.skip_fast) return;  // done by k1_bulk
+  if (fast) {
+    constexpr int R = 4;
+    const uint32_t sh = 4 * (lane & 7);
+    const int wsub = lane >> 3;
+    const bool stats = p.cmax != nullptr;
+    double acc = 0.0;
+    float cm = 0.0f;
+    for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+      float4 g[R], raw[R];
+      uint32_t wn[R], rn[R];
+      load_rows<R, true>(g, gin + r0 * kRowElems, lane, s);
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        raw[k] = ldg_rw(we + (r0 + k) * kRowElems + 4 * lane);
+        wn[k] = __ldg(pkp + 4 * (r0 + k) + wsub) >> sh;
+        rn[k] = MODE == 2 ? __ldg(rp + 4 * (r0 + k) + wsub) >> sh : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (MODE == 2 && !(isfinite(g[k].x) && isfinite(g[k].y) && isfinite(g[k].z) &&
+                           isfinite(g[k].w))) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (!isfinite(comp(g[k], q))) {
+              flag(p.err, kErrGrad,
+                   (static_cast<unsigned long long>(p.worker_base + w) << 40) |
+                       (kc + i0 + (r0 + k) * kRowElems + 4 * lane + q));
+            }
+          }
+        }
+        uint32_t nib = 0;
+        float4 rawn;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float v;
+          if (MODE == 0) {
+            v = comp(g[k], q);
+          } else {
+            const float mq = __fmul_rn((rn[k] >> q) & 1u ? pos_m : neg_m, IC);   // fusion.cpp:143
+            v = __fadd_rn(__fmul_rn(A, mq), __fmul_rn(B, comp(g[k], q)));     // kernels.cpp:253
+          }
+          const float rec = (wn[k] >> q) & 1u ? Sp : -Sp;
+          const float delta = __fsub_rn(comp(raw[k], q), rec);                // compression.cpp:194
+          const float corr = __fadd_rn(v, __fmul_rn(es, delta));              // :181
+          set_comp(rawn, q, __fadd_rn(v, delta));
+          nib |= static_cast<uint32_t>(corr >= 0.0f) << q;                    // :50
+          acc += fabs(static_cast<double>(corr));                              // :54
+          if (stats) {
+            const float ac = fabsf(corr);
+            cm = cm < ac ? ac : cm;
+          }
+        }
+        st4(we + (r0 + k) * kRowElems + 4 * lane, rawn);
+        stage_row_bits(sw, r0 + k, lane, nib);
+      }
+    }
+    const uint4 wv = tile_words(sw, lane);
+    reinterpret_cast<uint4*>(pkc)[lane] = wv;
+    if (rxw) reinterpret_cast<uint4*>(rxw)[lane] = wv;  // fused alltoall
+    acc = warp_bfly_sum(acc);
+    if (lane == 0) p.partials[ep * p.tpc + t] = acc;
+    if (stats) {
+      cm = warp_max(cm);
+      if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
+    }
+    return;
+  }
+
+  int l = 0;
+  int lcache = -1;
+  if (MODE != 0) l = find_layer(p.off, p.L, kc + i0);
+
+  clear_tile_words(sw, lane);  // rows past the chunk end keep zero bits
+  double acc = 0.0;
+  float cm = 0.0f;
+  for (int r = 0; r < kRowsPerTile; ++r) {
+    const uint64_t ir = i0 + static_cast<uint64_t>(r) * kRowElems;
+    if (ir >= p.c) break;
+    const uint64_t kr = kc + ir;
+    const float4 g = ld_row4<true>(gin + r * kRowElems, lane, s);
+    float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (MODE == 1) mv = ld_row4<false>(p.m + kr, lane, s);
+    const float4 raw = ld4(we + r * kRowElems + 4 * lane);
+    const uint32_t wnib = row_nibble(pkp, r, lane);
+    uint32_t rnib = 0;
+    if (MODE == 2) rnib = row_nibble(rp, r, lane);
+
+    // Stream value for each of the lane's 4 elements.
+    float4 sv;
+    if (MODE == 0) {
+      sv = g;
+    } else {
+      while (l < p.L && kr >= __ldg(p.off + l + 1)) ++l;
+      const bool uniform = l < p.L && kr + (kRowElems - 1) < __ldg(p.off + l + 1);
+      if (uniform && l != lcache) {
+        A = __ldg(p.A + l);
+        B = __ldg(p.B + l);
+        IC = __ldg(p.invc + l);
+        lcache = l;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float a = A, b = B, ic = IC;
+        bool pad = false;
+        if (!uniform) {
+          const uint64_t k = kr + 4 * lane + q;
+          int le = l;
+          while (le < p.L && k >= __ldg(p.off + le + 1)) ++le;
+          pad = le >= p.L;
+          if (!pad) {
+            a = __ldg(p.A + le);
+            b = __ldg(p.B + le);
+            ic = __ldg(p.invc + le);
+          }
+        }
+        float mq;
+        if (MODE == 1) mq = comp(mv, q);
+        else mq = __fmul_rn((rnib >> q) & 1u ? pos_m : neg_m, ic);  // fusion.cpp:143
+        // kernels.cpp:253  dst = a*x + b*y
+        const float v = pad ? 0.0f : __fadd_rn(__fmul_rn(a, mq), __fmul_rn(b, comp(g, q)));
+        set_comp(sv, q, v);
+      }
+    }
+    if (MODE != 0) {
+      // check_gradients (optimizers.cpp:99-117): flag, reported by the host.
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t k = kr + 4 * lane + q;
+        if (ir + 4 * lane + q < p.c && k < p.d && !isfinite(comp(g, q))) {
+          flag(p.err, kErrGrad,
+               (static_cast<unsigned long long>(p.worker_base + w) << 40) | k);
+        }
+      }
+    }
+
+    uint32_t nib = 0;
+    float4 rawn;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = ir + 4 * lane + q;
+      const uint64_t k = kc + i;
+      const float v = k < p.d ? comp(sv, q) : 0.0f;  // comm_sim.cpp:136-137 zero pad
+      const float rec = (wnib >> q) & 1u ? Sp : -Sp;
+      const float delta = __fsub_rn(comp(raw, q), rec);          // compression.cpp:194-195
+      const float corr = __fadd_rn(v, __fmul_rn(es, delta));     // :181 (1*v + es*delta)
+      const float rn = __fadd_rn(v, delta);                      // v + delta
+      const bool live = i < p.c;
+      set_comp(rawn, q, live ? rn : 0.0f);
+      if (live) {
+        nib |= static_cast<uint32_t>(corr >= 0.0f) << q;         // compression.cpp:50
+        acc += fabs(static_cast<double>(corr));                   // :54 sum_abs
+        const float ac = fabsf(corr);
+        cm = cm < ac ? ac : cm;
+      }
+    }
+    st4(we + r * kRowElems + 4 * lane, rawn);
+    stage_row_bits(sw, r, lane, nib);
+  }
+  {
+    const uint4 wv = tile_words(sw, lane);
+    reinterpret_cast<uint4*>(pkc)[lane] = wv;
+    if (rxw) reinterpret_cast<uint4*>(rxw)[lane] = wv;
+  }
+  acc = warp_bfly_sum(acc);
+  if (lane == 0) p.partials[ep * p.tpc + t] = acc;
+  if (p.cmax) {
+    cm = warp_max(cm);
+    if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
+  }
+}
+
 template <int MODE, bool ALIGNED>
 __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p) {
   __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
@@ -320,223 +536,7 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
       const long long wl = it / p.n_slow;
       tile = wl * per_w + __ldg(p.slow_list + (it - wl * p.n_slow));
     }
-    const int w = static_cast<int>(tile / per_w);
-    const long long rem = tile - w * per_w;
-    const int j = static_cast<int>(rem / p.tpc);
-    const int t = static_cast<int>(rem - static_cast<long long>(j) * p.tpc);
-    const uint64_t i0 = static_cast<uint64_t>(t) * kTile;  // chunk-relative
-    const uint64_t kc = static_cast<uint64_t>(j) * p.c;    // global chunk start
-    const int s = ALIGNED ? 0 : static_cast<int>(kc & 3u);  // ALIGNED: c % 4 == 0
-    const size_t ep = static_cast<size_t>(w) * p.n + j;    // endpoint (worker, chunk)
-    const float* gin = p.in + static_cast<size_t>(w) * p.in_stride + kc + i0;
-    float* we = p.werr + ep * p.c_pad + i0;
-    const uint32_t* pkp = p.pk_prev + ep * p.slot;
-    uint32_t* pkc = p.pk_cur + ep * p.slot + (i0 >> 5);
-    uint32_t* rxw = p.peer_rx ? p.peer_rx[j] + p.rx_off + (i0 >> 5) : nullptr;
-    const float Sp = slot_scale(pkp, p.W);
-    pkp += i0 >> 5;
-
-    float pos_m = 0.f, neg_m = 0.f;
-    const uint32_t* rp = nullptr;
-    if (MODE == 2) {
-      const uint32_t* rs = p.res_prev + static_cast<size_t>(j) * p.slot;
-      const float S2 = slot_scale(rs, p.W);
-      pos_m = S2;
-      neg_m = S2 == 0.0f ? 0.0f : -S2;
-      rp = rs + (i0 >> 5);
-    }
-    float A = 0.f, B = 0.f, IC = 0.f;
-
-    // Fast path: the whole tile lies inside the chunk, inside the real
-    // (unpadded) data and inside one layer.  Rows are processed 4 at a time
-    // with all loads issued first; same per-element arithmetic and the same
-    // accumulation order as the general path below.
-    bool fast = MODE != 1 && i0 + kTile <= p.c && kc + i0 + kTile <= p.d;
-    if (fast && MODE == 2) {
-      int l0;
-      if (p.tile_layer) {
-        l0 = __ldg(p.tile_layer + static_cast<size_t>(j) * p.tpc + t);
-        fast = l0 >= 0;
-      } else {
-        l0 = find_layer(p.off, p.L, kc + i0);
-        fast = l0 < p.L && kc + i0 + (kTile - 1) < __ldg(p.off + l0 + 1);
-      }
-      if (fast) {
-        A = __ldg(p.A + l0);
-        B = __ldg(p.B + l0);
-        IC = __ldg(p.invc + l0);
-      }
-    }
-    if (fast && p.skip_fast) continue;  // done by k1_bulk
-    if (fast) {
-      constexpr int R = 4;
-      const uint32_t sh = 4 * (lane & 7);
-      const int wsub = lane >> 3;
-      const bool stats = p.cmax != nullptr;
-      double acc = 0.0;
-      float cm = 0.0f;
-      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
-        float4 g[R], raw[R];
-        uint32_t wn[R], rn[R];
-        load_rows<R, true>(g, gin + r0 * kRowElems, lane, s);
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          raw[k] = ldg_rw(we + (r0 + k) * kRowElems + 4 * lane);
-          wn[k] = __ldg(pkp + 4 * (r0 + k) + wsub) >> sh;
-          rn[k] = MODE == 2 ? __ldg(rp + 4 * (r0 + k) + wsub) >> sh : 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          if (MODE == 2 && !(isfinite(g[k].x) && isfinite(g[k].y) && isfinite(g[k].z) &&
-                             isfinite(g[k].w))) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (!isfinite(comp(g[k], q))) {
-                flag(p.err, kErrGrad,
-                     (static_cast<unsigned long long>(p.worker_base + w) << 40) |
-                         (kc + i0 + (r0 + k) * kRowElems + 4 * lane + q));
-              }
-            }
-          }
-          uint32_t nib = 0;
-          float4 rawn;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float v;
-            if (MODE == 0) {
-              v = comp(g[k], q);
-            } else {
-              const float mq = __fmul_rn((rn[k] >> q) & 1u ? pos_m : neg_m, IC);   // fusion.cpp:143
-              v = __fadd_rn(__fmul_rn(A, mq), __fmul_rn(B, comp(g[k], q)));     // kernels.cpp:253
-            }
-            const float rec = (wn[k] >> q) & 1u ? Sp : -Sp;
-            const float delta = __fsub_rn(comp(raw[k], q), rec);                // compression.cpp:194
-            const float corr = __fadd_rn(v, __fmul_rn(es, delta));              // :181
-            set_comp(rawn, q, __fadd_rn(v, delta));
-            nib |= static_cast<uint32_t>(corr >= 0.0f) << q;                    // :50
-            acc += fabs(static_cast<double>(corr));                              // :54
-            if (stats) {
-              const float ac = fabsf(corr);
-              cm = cm < ac ? ac : cm;
-            }
-          }
-          st4(we + (r0 + k) * kRowElems + 4 * lane, rawn);
-          stage_row_bits(sw, r0 + k, lane, nib);
-        }
-      }
-      const uint4 wv = tile_words(sw, lane);
-      reinterpret_cast<uint4*>(pkc)[lane] = wv;
-      if (rxw) reinterpret_cast<uint4*>(rxw)[lane] = wv;  // fused alltoall
-      acc = warp_bfly_sum(acc);
-      if (lane == 0) p.partials[ep * p.tpc + t] = acc;
-      if (stats) {
-        cm = warp_max(cm);
-        if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
-      }
-      continue;
-    }
-
-    int l = 0;
-    int lcache = -1;
-    if (MODE != 0) l = find_layer(p.off, p.L, kc + i0);
-
-    clear_tile_words(sw, lane);  // rows past the chunk end keep zero bits
-    double acc = 0.0;
-    float cm = 0.0f;
-    for (int r = 0; r < kRowsPerTile; ++r) {
-      const uint64_t ir = i0 + static_cast<uint64_t>(r) * kRowElems;
-      if (ir >= p.c) break;
-      const uint64_t kr = kc + ir;
-      const float4 g = ld_row4<true>(gin + r * kRowElems, lane, s);
-      float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (MODE == 1) mv = ld_row4<false>(p.m + kr, lane, s);
-      const float4 raw = ld4(we + r * kRowElems + 4 * lane);
-      const uint32_t wnib = row_nibble(pkp, r, lane);
-      uint32_t rnib = 0;
-      if (MODE == 2) rnib = row_nibble(rp, r, lane);
-
-      // Stream value for each of the lane's 4 elements.
-      float4 sv;
-      if (MODE == 0) {
-        sv = g;
-      } else {
-        while (l < p.L && kr >= __ldg(p.off + l + 1)) ++l;
-        const bool uniform = l < p.L && kr + (kRowElems - 1) < __ldg(p.off + l + 1);
-        if (uniform && l != lcache) {
-          A = __ldg(p.A + l);
-          B = __ldg(p.B + l);
-          IC = __ldg(p.invc + l);
-          lcache = l;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float a = A, b = B, ic = IC;
-          bool pad = false;
-          if (!uniform) {
-            const uint64_t k = kr + 4 * lane + q;
-            int le = l;
-            while (le < p.L && k >= __ldg(p.off + le + 1)) ++le;
-            pad = le >= p.L;
-            if (!pad) {
-              a = __ldg(p.A + le);
-              b = __ldg(p.B + le);
-              ic = __ldg(p.invc + le);
-            }
-          }
-          float mq;
-          if (MODE == 1) mq = comp(mv, q);
-          else mq = __fmul_rn((rnib >> q) & 1u ? pos_m : neg_m, ic);  // fusion.cpp:143
-          // kernels.cpp:253  dst = a*x + b*y
-          const float v = pad ? 0.0f : __fadd_rn(__fmul_rn(a, mq), __fmul_rn(b, comp(g, q)));
-          set_comp(sv, q, v);
-        }
-      }
-      if (MODE != 0) {
-        // check_gradients (optimizers.cpp:99-117): flag, reported by the host.
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint64_t k = kr + 4 * lane + q;
-          if (ir + 4 * lane + q < p.c && k < p.d && !isfinite(comp(g, q))) {
-            flag(p.err, kErrGrad,
-                 (static_cast<unsigned long long>(p.worker_base + w) << 40) | k);
-          }
-        }
-      }
-
-      uint32_t nib = 0;
-      float4 rawn;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint64_t i = ir + 4 * lane + q;
-        const uint64_t k = kc + i;
-        const float v = k < p.d ? comp(sv, q) : 0.0f;  // comm_sim.cpp:136-137 zero pad
-        const float rec = (wnib >> q) & 1u ? Sp : -Sp;
-        const float delta = __fsub_rn(comp(raw, q), rec);          // compression.cpp:194-195
-        const float corr = __fadd_rn(v, __fmul_rn(es, delta));     // :181 (1*v + es*delta)
-        const float rn = __fadd_rn(v, delta);                      // v + delta
-        const bool live = i < p.c;
-        set_comp(rawn, q, live ? rn : 0.0f);
-        if (live) {
-          nib |= static_cast<uint32_t>(corr >= 0.0f) << q;         // compression.cpp:50
-          acc += fabs(static_cast<double>(corr));                   // :54 sum_abs
-          const float ac = fabsf(corr);
-          cm = cm < ac ? ac : cm;
-        }
-      }
-      st4(we + r * kRowElems + 4 * lane, rawn);
-      stage_row_bits(sw, r, lane, nib);
-    }
-    {
-      const uint4 wv = tile_words(sw, lane);
-      reinterpret_cast<uint4*>(pkc)[lane] = wv;
-      if (rxw) reinterpret_cast<uint4*>(rxw)[lane] = wv;
-    }
-    acc = warp_bfly_sum(acc);
-    if (lane == 0) p.partials[ep * p.tpc + t] = acc;
-    if (p.cmax) {
-      cm = warp_max(cm);
-      if (lane == 0) p.cmax[ep * p.tpc + t] = cm;
-    }
+    k1_tile<MODE, ALIGNED>(p, tile, lane, sw, es);
   }
   if (p.peer_rx) warp_fence_system(threadIdx.x & 31);  // remote words before the finalize signal
 }
@@ -675,6 +675,15 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
   for (int s = 0; s < kBulkStages; ++s) {
     issue(s, ptile, pr);
     advance(ptile, pr);
+  }
+  // Boundary tiles (layer boundaries, chunk/padding ends) take the general
+  // path here, while the prologue copies are in flight.
+  if (p.slow_list) {
+    const long long stotal = static_cast<long long>(p.n_slow) * p.nw;
+    for (long long it = gw; it < stotal; it += nwarps) {
+      const long long wl = it / p.n_slow;
+      k1_tile<MODE, false>(p, wl * per_w + __ldg(p.slow_list + (it - wl * p.n_slow)), lane, sw, es);
+    }
   }
 
   long long ctile = next_fast(gw);
@@ -1711,13 +1720,10 @@ int launch_k1_phase(const K1Params& p, int mode, int phase, cudaStream_t s) {
     if (bulk_rows() == 4) return mode == 0 ? launch_k1_bulk<0, 4>(p, s) : launch_k1_bulk<2, 4>(p, s);
     return mode == 0 ? launch_k1_bulk<0, 8>(p, s) : launch_k1_bulk<2, 8>(p, s);
   }
-  K1Params q = p;
-  q.skip_fast = 1;
-  if (q.slow_list && q.n_slow == 0) return 0;
-  const int g = resident(k1_worker_compress<2, false>, 148 * 16);
-  if (mode == 0) k1_worker_compress<0, false><<<g, kBlock, 0, s>>>(q);
-  else k1_worker_compress<2, false><<<g, kBlock, 0, s>>>(q);
-  return 1;
+  (void)p;
+  (void)mode;
+  (void)s;
+  return 0;  // the boundary tiles run inside k1_bulk
 }
 
 int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
@@ -1725,21 +1731,7 @@ int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
     // Misaligned chunks: fast tiles through the bulk-copy pipeline (g staged
     // with alignment slack), then the boundary tiles through the general
     // kernel.  Aligned chunks stay on the register path, which measures faster.
-    int k;
-    if (bulk_rows() == 4) k = mode == 0 ? launch_k1_bulk<0, 4>(p, s) : launch_k1_bulk<2, 4>(p, s);
-    else k = mode == 0 ? launch_k1_bulk<0, 8>(p, s) : launch_k1_bulk<2, 8>(p, s);
-    K1Params q = p;
-    q.skip_fast = 1;
-    if (q.slow_list && q.n_slow == 0) return k;  // no boundary tiles
-    const bool al = (p.c & 3u) == 0;
-    if (mode == 0) {
-      if (al) k1_worker_compress<0, true><<<resident(k1_worker_compress<0, true>, grid), kBlock, 0, s>>>(q);
-      else k1_worker_compress<0, false><<<resident(k1_worker_compress<0, false>, grid), kBlock, 0, s>>>(q);
-    } else {
-      if (al) k1_worker_compress<2, true><<<resident(k1_worker_compress<2, true>, grid), kBlock, 0, s>>>(q);
-      else k1_worker_compress<2, false><<<resident(k1_worker_compress<2, false>, grid), kBlock, 0, s>>>(q);
-    }
-    return k + 1;
+    return launch_k1_phase(p, mode, 0, s);
   }
   K1Params full = p;  // register path: every tile, the slow list does not apply
   full.slow_list = nullptr;
