@@ -1686,12 +1686,13 @@ int launch_k1_bulk(const K1Params& p, cudaStream_t s) {
   return 1;
 }
 
-// Rows per bulk stage (BL_K1_BULK_R=4|8, default 8) and whether aligned
-// chunks also take the bulk path (BL_K1_BULK=all) — tuning knobs.
+// Rows per bulk stage (BL_K1_BULK_R=4|8, default 4: 4 blocks of 4 warps per
+// SM; 8 halves the resident warps) and whether aligned chunks also take the
+// bulk path (BL_K1_BULK=all|none) — tuning knobs.
 static int bulk_rows() {
   static const int r = [] {
     const char* e = std::getenv("BL_K1_BULK_R");
-    return e && std::atoi(e) == 4 ? 4 : 8;
+    return e && std::atoi(e) == 8 ? 8 : 4;
   }();
   return r;
 }
