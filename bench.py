@@ -116,6 +116,9 @@ def algorithmic_bytes(d: int, n: int, nw: int) -> dict:
     c = P // n
     ns = nw
     return {
+        # warmup stage: W1 g, m r/w, v r/w, x (24d); W2 m, v, x r/w (16d)
+        "w1_warmup_a": 24 * d,
+        "w2_warmup_b": 16 * d,
         # g (4d) + werr r/w (8P) + prev worker packet, prev result packet, new packet (3P/8)
         "k1_worker_compress": nw * (4 * d + 8 * P + 3 * P / 8),
         # serr r/w (8c) + n worker packets + prev server packet + new packet
@@ -199,6 +202,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
                     help="NCCL-mode packet exchange: fused NVLink peer stores or NCCL")
+    ap.add_argument("--stage", default="compression", choices=["compression", "warmup"],
+                    help="time compression-stage steps (headline) or warmup LAMB steps")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
 
@@ -252,7 +257,8 @@ def main():
         cl = bl.SimCluster(n, d, device=local, stream=stream.cuda_stream)
     nw = cl.local_workers()
     total_steps = 2 + args.warmup + 2 * args.steps + 8
-    hp = bl.HyperParams(total_steps=total_steps, warmup_steps=2)
+    hp = bl.HyperParams(total_steps=total_steps,
+                        warmup_steps=2 if args.stage == "compression" else total_steps)
     opt = bl.Optimizer("onebit_lamb", layout, hp, cl)
 
     # synthetic state and gradients (x0 ~ N(0, 0.02^2); g ~ N(0, sigma_l^2))
@@ -367,7 +373,8 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC if args.workload == "bert-large" else f"1-bit LAMB step time, {args.workload}",
+            "metric": (METRIC if args.workload == "bert-large" else f"1-bit LAMB step time, {args.workload}")
+            if args.stage == "compression" else f"warmup LAMB step time, {args.workload}",
             "value": ms, "unit": "ms", "n_gpus": args.gpus if world == 1 else world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None,

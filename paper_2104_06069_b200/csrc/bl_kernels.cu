@@ -1358,6 +1358,50 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
     const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
     const int s = static_cast<int>(lo & 3u);
     double ax = 0.0, au = 0.0, av = 0.0, am = 0.0;
+    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len) {
+      // Fast path: aligned full tile, 4 rows per batch, loads issued first.
+      constexpr int R = 4;
+      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        float4 g[R], m[R], v[R], x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
+          g[k] = ldg_ro(p.gbar + o);
+          m[k] = ldg_rw(p.m + o);
+          v[k] = ldg_rw(p.v + o);
+          x[k] = ldg_ro(p.x + o);
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          if (p.err && !(isfinite(g[k].x) && isfinite(g[k].y) && isfinite(g[k].z) && isfinite(g[k].w))) {
+            for (int q = 0; q < 4; ++q)
+              if (!isfinite(comp(g[k], q)))
+                flag(p.err, kErrGrad, (static_cast<unsigned long long>(p.worker_base) << 40) |
+                                          (base + (r0 + k) * kRowElems + 4 * lane + q));
+          }
+          float4 mn, vn;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float gq = comp(g[k], q);
+            const float mq = __fadd_rn(__fmul_rn(p.b1, comp(m[k], q)), __fmul_rn(p.omb1, gq));
+            const float vq =
+                __fadd_rn(__fmul_rn(p.b2, comp(v[k], q)), __fmul_rn(__fmul_rn(p.omb2, gq), gq));
+            set_comp(mn, q, mq);
+            set_comp(vn, q, vq);
+            float u = __fdiv_rn(mq, __fadd_rn(__fsqrt_rn(vq), p.eta));
+            if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
+            const double xd = comp(x[k], q), ud = u, vd = vq;
+            ax += xd * xd;
+            au += ud * ud;
+            av += vd * vd;
+            am += fabs(static_cast<double>(mq));
+          }
+          const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
+          st4(p.m + o, mn);
+          st4(p.v + o, vn);
+        }
+      }
+    } else
     for (int r = 0; r < kRowsPerTile; ++r) {
       const uint64_t ir = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r) * kRowElems;
       if (ir >= len) break;
@@ -1371,6 +1415,9 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float gq = comp(g, q);
+        if (p.err && q < nv && !isfinite(gq))
+          flag(p.err, kErrGrad, (static_cast<unsigned long long>(p.worker_base) << 40) |
+                                    (kr + 4 * lane + q));
         // kernels.cpp:238 axpby y = a*y + b*x ; :245 axpby_square
         const float mq = __fadd_rn(__fmul_rn(p.b1, comp(m, q)), __fmul_rn(p.omb1, gq));
         const float vq = __fadd_rn(__fmul_rn(p.b2, comp(v, q)), __fmul_rn(__fmul_rn(p.omb2, gq), gq));
@@ -1494,6 +1541,33 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
     const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
     const int s = static_cast<int>(lo & 3u);
     const float a = __ldg(p.coef_x + l);
+    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len) {
+      constexpr int R = 4;
+      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        float4 m[R], v[R], x[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
+          m[k] = ldg_ro(p.m + o);
+          v[k] = ldg_ro(p.v + o);
+          x[k] = ldg_rw(p.x + o);
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          float4 xn;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float u = __fdiv_rn(comp(m[k], q), __fadd_rn(__fsqrt_rn(comp(v[k], q)), p.eta));
+            if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
+            set_comp(xn, q, __fadd_rn(comp(x[k], q), __fmul_rn(a, u)));
+          }
+          const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
+          st4(p.x + o, xn);
+          if (p.finalize) st4(p.vf + o, v[k]);  // optimizers.cpp:205
+        }
+      }
+      continue;
+    }
     for (int r = 0; r < kRowsPerTile; ++r) {
       const uint64_t ir = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r) * kRowElems;
       if (ir >= len) break;

@@ -181,6 +181,8 @@ struct W1Params {
   float b1, omb1, b2, omb2, eta, wd;
   double* tile_sums;  // [tiles][4]: x^2, u^2, v^2, |m|
   int adam;           // adam_step: no norms needed (kept for the trace)
+  unsigned long long* err;  // non-null: gbar IS the single worker's gradient -> finite check
+  int worker_base;
 };
 
 struct WEpiParams {

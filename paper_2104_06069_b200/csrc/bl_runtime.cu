@@ -484,12 +484,16 @@ void bl_cluster::sync_and_check(const std::vector<uint64_t>* off) {
 // bl_optimizer
 // ---------------------------------------------------------------------------
 void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, bool adam) {
-  cl->lossless(true);  // average_lossless (optimizers.cpp:119-138)
-  cl->ledger_lossless();
+  // average_lossless (optimizers.cpp:119-138).  With one worker the average
+  // (float)((0.0 + g) * 1.0) is g itself: W1 reads the gradient in place and
+  // only the finite check runs.
+  const bool single = cl->n == 1;
   cudaEvent_t a;
+  if (!single) cl->lossless(true);
+  cl->ledger_lossless();
   W1Params w1{};
   w1.lt = lt();
-  w1.gbar = cl->out;
+  w1.gbar = single ? cl->in : cl->out;
   w1.m = m;
   w1.v = v;
   w1.x = x;
@@ -501,6 +505,8 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   w1.wd = static_cast<float>(hp.weight_decay);
   w1.tile_sums = tile_sums;
   w1.adam = adam ? 1 : 0;
+  w1.err = single ? cl->err : nullptr;  // check_gradients fused into W1
+  w1.worker_base = cl->rank;
   cl->begin(KC_W1, &a);
   cl->end(KC_W1, a, launch_w1(w1, cl->grid(tiles), cl->stream));
 
