@@ -840,10 +840,14 @@ __device__ __forceinline__ void flush_server_words(const K3Params& p, uint32_t* 
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kBlock, (NT > 0 && NT <= 2) ? 4 : 2) k3_server_reduce(const K3Params p) {
+__global__ void __launch_bounds__(kBlock, NT == 1 ? 4 : (NT == 2 ? 3 : 2)) k3_server_reduce(const K3Params p) {
   __shared__ float s_scale[kWarpsPerBlock][64];
   __shared__ uint32_t* s_peer[64];
   __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
+  // 2^n-entry server-average table for n in {4, 8} (per warp, per chunk)
+  constexpr bool kTable = NT >= 4;
+  __shared__ float s_tab[kWarpsPerBlock][kTable ? (1 << (NT > 0 ? NT : 1)) : 1];
+  int tab_chunk = -1;
   uint32_t* sw = s_words[threadIdx.x >> 5];
   const int n = NT > 0 ? NT : p.n;
   if (p.peer_res) {
@@ -893,22 +897,53 @@ __global__ void __launch_bounds__(kBlock, (NT > 0 && NT <= 2) ? 4 : 2) k3_server
           for (int i = 0; i < (NT > 0 ? NT : 1); ++i)
             wn[k][i] = ld_cg(inw + i * p.in_i + 4 * (r0 + k) + wsub) >> sh;
         }
+      if (kTable && tab_chunk != j) {
+        // avg(pattern) for every n-bit sign pattern of chunk j: the same
+        // ascending fp64 sum (skipping S == 0) and *1/n as the direct form.
+        __syncwarp();
+        for (int e = lane; e < (1 << NT); e += 32) {
+          double acc = 0.0;
+#pragma unroll
+          for (int i = 0; i < NT; ++i) {
+            const float S = s_scale[wib][i];
+            if (S != 0.0f) acc += ((e >> i) & 1) ? static_cast<double>(S) : -static_cast<double>(S);
+          }
+          s_tab[wib][e] = static_cast<float>(acc * inv_n);
+        }
+        __syncwarp();
+        tab_chunk = j;
+      }
 #pragma unroll
         for (int k = 0; k < R; ++k) {
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          float4 avg;
+          if (kTable) {
+            uint32_t x = 0;  // nibble of worker i at bits 4i..4i+3
 #pragma unroll
-          for (int i = 0; i < (NT > 0 ? NT : 1); ++i) {  // compression.cpp:83-89
-            const float S = s_scale[wib][i];
-            if (S != 0.0f) {
-              const double Sd = S;
-              a0 += (wn[k][i] & 1u) ? Sd : -Sd;
-              a1 += (wn[k][i] & 2u) ? Sd : -Sd;
-              a2 += (wn[k][i] & 4u) ? Sd : -Sd;
-              a3 += (wn[k][i] & 8u) ? Sd : -Sd;
+            for (int i = 0; i < NT; ++i) x |= (wn[k][i] & 0xFu) << (4 * i);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // gather bits q, q+4, ... -> n-bit pattern
+              uint32_t y = (x >> q) & 0x11111111u;
+              y = (y | (y >> 3)) & 0x03030303u;
+              y = (y | (y >> 6)) & 0x000F000Fu;
+              y = (y | (y >> 12)) & 0xFFu;
+              set_comp(avg, q, s_tab[wib][y]);
             }
+          } else {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+            for (int i = 0; i < (NT > 0 ? NT : 1); ++i) {  // compression.cpp:83-89
+              const float S = s_scale[wib][i];
+              if (S != 0.0f) {
+                const double Sd = S;
+                a0 += (wn[k][i] & 1u) ? Sd : -Sd;
+                a1 += (wn[k][i] & 2u) ? Sd : -Sd;
+                a2 += (wn[k][i] & 4u) ? Sd : -Sd;
+                a3 += (wn[k][i] & 8u) ? Sd : -Sd;
+              }
+            }
+            avg = make_float4(static_cast<float>(a0 * inv_n), static_cast<float>(a1 * inv_n),
+                              static_cast<float>(a2 * inv_n), static_cast<float>(a3 * inv_n));
           }
-          const float4 avg = make_float4(static_cast<float>(a0 * inv_n), static_cast<float>(a1 * inv_n),
-                                         static_cast<float>(a2 * inv_n), static_cast<float>(a3 * inv_n));
           uint32_t nib = 0;
           float4 rawn;
 #pragma unroll
@@ -1590,6 +1625,42 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
 }
 
 // Lossless average (comm_sim.cpp:214-222): ascending workers in fp64, * 1/n.
+// Vector form: 4 elements per thread with 128-bit loads (inputs are 16-byte
+// aligned library buffers), any output alignment.
+__global__ void k_average4(const float* in, uint64_t stride, int n, uint64_t len, float* out,
+                           unsigned long long* err, int check, int worker_base) {
+  const double inv_n = 1.0 / static_cast<double>(n);
+  const uint64_t n4 = len / 4;
+  for (uint64_t k4 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k4 < n4;
+       k4 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < n; ++i) {
+      const float4 g = ldg_ro(in + static_cast<size_t>(i) * stride + 4 * k4);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float gq = comp(g, q);
+        if (check && !isfinite(gq))
+          flag(err, kErrGrad, (static_cast<unsigned long long>(worker_base + i) << 40) | (4 * k4 + q));
+        a[q] += static_cast<double>(gq);
+      }
+    }
+    if (out) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) out[4 * k4 + q] = static_cast<float>(a[q] * inv_n);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < len - 4 * n4) {  // tail
+    const uint64_t k = 4 * n4 + threadIdx.x;
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const float g = in[static_cast<size_t>(i) * stride + k];
+      if (check && !isfinite(g)) flag(err, kErrGrad, (static_cast<unsigned long long>(worker_base + i) << 40) | k);
+      acc += static_cast<double>(g);
+    }
+    if (out) out[k] = static_cast<float>(acc * inv_n);
+  }
+}
+
 __global__ void k_average(const float* in, uint64_t stride, int n, uint64_t len, float* out,
                           unsigned long long* err, int check, int worker_base) {
   const double inv_n = 1.0 / static_cast<double>(n);
@@ -1872,8 +1943,14 @@ int launch_w2(const W2Params& p, int grid, cudaStream_t s) {
 
 int launch_average(const float* in, uint64_t stride, int n, uint64_t len, float* out,
                    unsigned long long* err, int check_finite, int worker_base, cudaStream_t s) {
-  k_average<<<grid_for_elems(len), 256, 0, s>>>(in, stride, n, len, out, err, check_finite,
-                                                 worker_base);
+  const bool vec = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && stride % 4 == 0;
+  if (vec) {
+    k_average4<<<grid_for_elems(len / 4 + 1), 256, 0, s>>>(in, stride, n, len, out, err, check_finite,
+                                                          worker_base);
+  } else {
+    k_average<<<grid_for_elems(len), 256, 0, s>>>(in, stride, n, len, out, err, check_finite,
+                                                   worker_base);
+  }
   return 1;
 }
 
