@@ -367,6 +367,15 @@ class SimCluster:
                                                     error_scale, mem))
         return res[: self._dim]
 
+    def compressed_allreduce_resident(self, out, error_scale: float = 1.0):
+        """compressed_allreduce on the streams already in the cluster's input
+        buffers (zero-copy); `out` is a torch CUDA tensor of dim floats."""
+        nw = self.local_workers()
+        ptrs = (C.c_void_p * nw)(*[self.input_buffer(i) for i in range(nw)])
+        _check(_lib.bl_cluster_compressed_allreduce(self._h, ptrs, nw, self._dim, out.data_ptr(),
+                                                    error_scale, MEM_DEVICE))
+        return out
+
     def lossless_allreduce(self, inputs):
         """comm_sim.hpp:102."""
         ptrs, n_in, mem, keep, length = _pointers(inputs, self._dim)
