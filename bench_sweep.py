@@ -49,7 +49,10 @@ def main():
     rank, world, local = D.env_rank()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    stream = torch.cuda.current_stream()
+    # A real stream: the default stream's handle is NULL, which the library
+    # would replace by its own stream, escaping the events below.
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     for mb in [int(x) for x in args.sizes_mb.split(",")]:
         d = mb * (1 << 18)
         x = torch.randn(d, device="cuda", dtype=torch.float32)
