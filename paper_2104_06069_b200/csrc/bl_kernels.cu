@@ -1677,14 +1677,29 @@ __global__ void k_average(const float* in, uint64_t stride, int n, uint64_t len,
   }
 }
 
+// Result of the collective (compression.cpp:68-81, comm_sim.cpp:173,202):
+// chunk-relative, one warp per 32 packet words (1024 elements): every lane
+// reads the same word (broadcast) and writes one element of each 32-element
+// group (coalesced), truncated at c and d.
 __global__ void k_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
                              uint64_t d, float* out) {
-  const BitCursor bc{res, c, slot, W, n};
-  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < d;
-       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    float S;
-    const uint32_t b = bit_at(bc, k, &S);
-    out[k] = dec_value(b, S);
+  const int lane = threadIdx.x & 31;
+  const uint64_t groups = (W + 31) / 32;  // 32-word groups per chunk
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t g = gw; g < groups * n; g += nwarps) {
+    const uint64_t j = g / groups, w0 = (g - j * groups) * 32;
+    const uint32_t* sl = res + j * slot;
+    const float S = slot_scale_cg(sl, W);
+    const float pos = S, neg = S == 0.0f ? 0.0f : -S;
+    const uint64_t kc = j * c;
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) {
+      const uint64_t e = (w0 + i) * 32 + lane;  // chunk-relative element
+      if (e >= c || kc + e >= d) break;
+      const uint32_t word = __ldcg(sl + w0 + i);
+      out[kc + e] = (word >> lane) & 1u ? pos : neg;
+    }
   }
 }
 
@@ -1956,7 +1971,7 @@ int launch_average(const float* in, uint64_t stride, int n, uint64_t len, float*
 
 int launch_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
                       uint64_t d, float* out, cudaStream_t s) {
-  k_decompress<<<grid_for_elems(d), 256, 0, s>>>(res, n, c, slot, W, d, out);
+  k_decompress<<<grid_for_elems(d / 128 + 1), 256, 0, s>>>(res, n, c, slot, W, d, out);
   return 1;
 }
 
