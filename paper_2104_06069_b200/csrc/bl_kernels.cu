@@ -1693,12 +1693,12 @@ __global__ void k_decompress(const uint32_t* res, int n, uint64_t c, uint64_t sl
     const float S = slot_scale_cg(sl, W);
     const float pos = S, neg = S == 0.0f ? 0.0f : -S;
     const uint64_t kc = j * c;
-#pragma unroll 4
+    const uint32_t mine = __ldcg(sl + w0 + lane);  // one coalesced 128-B word load per warp
+#pragma unroll 8
     for (int i = 0; i < 32; ++i) {
+      const uint32_t word = __shfl_sync(FULL, mine, i);
       const uint64_t e = (w0 + i) * 32 + lane;  // chunk-relative element
-      if (e >= c || kc + e >= d) break;
-      const uint32_t word = __ldcg(sl + w0 + i);
-      out[kc + e] = (word >> lane) & 1u ? pos : neg;
+      if (e < c && kc + e < d) out[kc + e] = (word >> lane) & 1u ? pos : neg;
     }
   }
 }
