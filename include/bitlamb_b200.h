@@ -86,7 +86,9 @@ typedef struct bl_cluster_config {
   uint64_t dim;
   int32_t compressor; /* bl_compressor */
   int32_t baseline_bits_per_element;
-  int32_t verify_compensation; /* accepted; the identity is checked by the tests */
+  int32_t verify_compensation; /* re-check v + d_prev == dec + d_new on the device after every
+                                  collective with error_scale == 1 (comm_sim.cpp:83-106);
+                                  the fp32 path needs a tolerance >= 2^-23 */
   int32_t endpoint_stats;      /* refresh EndpointStats every collective (extra pass) */
   double compensation_tolerance;
   const uint8_t* nccl_unique_id; /* BL_NCCL_UNIQUE_ID_BYTES, BL_MODE_NCCL only */
@@ -189,6 +191,8 @@ float* bl_cluster_input_buffer(bl_cluster* c, int32_t worker);
 /* Instrumentation: number of kernels this object launched, and optional
  * CUDA-event timing per kernel class (names[k], total ms, launches). */
 uint64_t bl_cluster_kernel_launches(const bl_cluster* c);
+/* compensation_checks() (comm_sim.hpp:110): endpoints verified on this rank. */
+uint64_t bl_cluster_compensation_checks(const bl_cluster* c);
 bl_status bl_cluster_set_profiling(bl_cluster* c, int32_t on);
 int32_t bl_cluster_profile(bl_cluster* c, const char** names, double* total_ms,
                            uint64_t* launches, int32_t cap);

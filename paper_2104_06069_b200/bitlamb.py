@@ -131,6 +131,8 @@ def _load() -> C.CDLL:
     so.bl_cluster_input_buffer.restype = P
     so.bl_cluster_kernel_launches.argtypes = [P]
     so.bl_cluster_kernel_launches.restype = u64
+    so.bl_cluster_compensation_checks.argtypes = [P]
+    so.bl_cluster_compensation_checks.restype = u64
     so.bl_cluster_set_profiling.argtypes = [P, i32]
     so.bl_cluster_profile.argtypes = [P, P, P, P, i32]
     so.bl_cluster_profile.restype = i32
@@ -291,7 +293,7 @@ class SimCluster:
                  baseline_bits_per_element: int = 16, *, mode: str = "sim", rank: int = 0,
                  device: int = 0, nccl_unique_id: bytes | None = None, stream=None,
                  endpoint_stats: bool = False, verify_compensation: bool = False,
-                 transport: str = "auto"):
+                 compensation_tolerance: float = 1e-12, transport: str = "auto"):
         cfg = _ClusterConfig()
         cfg.n_workers = n_workers
         cfg.mode = 0 if mode == "sim" else 1
@@ -302,7 +304,7 @@ class SimCluster:
         cfg.baseline_bits_per_element = baseline_bits_per_element
         cfg.verify_compensation = int(verify_compensation)
         cfg.endpoint_stats = int(endpoint_stats)
-        cfg.compensation_tolerance = 1e-12
+        cfg.compensation_tolerance = compensation_tolerance
         self._uid = None
         if nccl_unique_id is not None:
             self._uid = (C.c_uint8 * 128).from_buffer_copy(nccl_unique_id)
@@ -441,6 +443,9 @@ class SimCluster:
 
     def synchronize(self) -> None:
         _check(_lib.bl_cluster_synchronize(self._h))
+
+    def compensation_checks(self) -> int:
+        return int(_lib.bl_cluster_compensation_checks(self._h))
 
     def kernel_launches(self) -> int:
         return int(_lib.bl_cluster_kernel_launches(self._h))

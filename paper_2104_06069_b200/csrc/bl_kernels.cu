@@ -1785,6 +1785,25 @@ __global__ void __launch_bounds__(1024) k_error_stats_final(const double* part, 
 
 __global__ void k_set_float(float* p, float v) { *p = v; }
 
+__global__ void k_verify(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot,
+                         uint64_t W, uint64_t c, uint64_t len, double tol, unsigned long long* err) {
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t j = k / c, i = k - j * c;
+    const uint32_t* sl = pk + j * slot;
+    const float S = slot_scale(sl, W);
+    const uint32_t b = (__ldg(sl + (i >> 5)) >> (i & 31)) & 1u;
+    const float r = raw[j * c_pad + i];             // corrected (es == 1)
+    const float dn = __fsub_rn(r, b ? S : -S);      // delta_new (compression.cpp:194-195)
+    const double lhs = r, dec = dec_value(b, S);    // decompress (compression.cpp:68-81)
+    const double rhs = dec + static_cast<double>(dn);
+    double den = fabs(lhs);
+    den = fabs(dec) > den ? fabs(dec) : den;
+    den = den < 1e-300 ? 1e-300 : den;
+    if (fabs(lhs - rhs) > tol * den) flag(err, kErrVerify, i);
+  }
+}
+
 // Stream-ordered wait for n peer signals (fused NVLink exchange).
 __global__ void k_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
                              unsigned long long* err) {
@@ -2008,6 +2027,12 @@ int launch_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const fl
 int launch_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
                       unsigned long long* err, cudaStream_t s) {
   k_wait_peers<<<1, 32, 0, s>>>(flags, n, epoch, err);
+  return 1;
+}
+
+int launch_verify(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot, uint64_t W,
+                  uint64_t c, uint64_t len, double tol, unsigned long long* err, cudaStream_t s) {
+  k_verify<<<grid_for_elems(len), 256, 0, s>>>(raw, c_pad, pk, slot, W, c, len, tol, err);
   return 1;
 }
 

@@ -26,7 +26,8 @@ enum ErrSlot : int {
   kErrScale = 1,   // non-finite compression scale: key = endpoint id
   kErrRecon = 2,   // non-finite reconstructed gradient: key = layer
   kErrPeer = 3,    // peer signal timeout (fused NVLink exchange): key = peer rank
-  kErrSlots = 4,
+  kErrVerify = 4,  // compensation identity violated: key = chunk-relative element
+  kErrSlots = 5,
 };
 
 // K1: worker compression of `nw` local streams, each split into n chunks.
@@ -246,6 +247,11 @@ int launch_error_stats(const float* raw, uint64_t c_pad, const uint32_t* pk, uin
                        uint64_t W, uint64_t c, uint64_t len, double* scratch, int scratch_tiles,
                        float* scratch_max, double* out, cudaStream_t s);
 int launch_set_float(float* p, float v, cudaStream_t s);
+// verify_compensation (comm_sim.cpp:83-106) for es == 1: for every element of
+// `len` flat (chunked) positions, corrected (= raw) against decompressed +
+// delta_new in fp64 with relative tolerance tol.
+int launch_verify(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot, uint64_t W,
+                  uint64_t c, uint64_t len, double tol, unsigned long long* err, cudaStream_t s);
 // Block the stream until flags[0..n) >= epoch (peer signals, bounded wait).
 int launch_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
                       unsigned long long* err, cudaStream_t s);

@@ -284,6 +284,7 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
   calls += 1;
   last_identity = false;
   ledger_compressed();
+  if (cfg.verify_compensation && (es_dev == nullptr ? es_host == 1.0f : verify_es_one)) verify_last();
   if (cfg.endpoint_stats) refresh_stats();
 }
 
@@ -395,6 +396,30 @@ void bl_cluster::lossless(bool check_finite) {
   end(KC_AG, a, 0);
 }
 
+// verify_compensation (comm_sim.cpp:83-106, 145-147, 170-172): after a
+// collective with error_scale == 1 every local worker chunk and local server
+// chunk is re-checked on the device; the count follows comm_sim.cpp:198-200
+// (n^2 + n per collective in SIM mode, n + 1 local endpoints in NCCL mode).
+void bl_cluster::verify_last() {
+  const int latest = static_cast<int>((calls + 1u) & 1u);
+  const double tol = cfg.compensation_tolerance;
+  cudaEvent_t a;
+  for (int w = 0; w < nw; ++w) {
+    begin(KC_STATS, &a);
+    end(KC_STATS, a,
+        launch_verify(werr + static_cast<size_t>(w) * n * c_pad, c_pad,
+                      wpk[latest] + static_cast<size_t>(w) * n * slot, slot, W, c, P, tol, err, stream));
+  }
+  for (int sv = 0; sv < ns; ++sv) {
+    const int j = mode == BL_MODE_SIM ? sv : rank;
+    begin(KC_STATS, &a);
+    end(KC_STATS, a,
+        launch_verify(serr + static_cast<size_t>(sv) * c_pad, c_pad,
+                      res[latest] + static_cast<size_t>(j) * slot, slot, W, c, c, tol, err, stream));
+  }
+  checks += static_cast<uint64_t>(nw) * n + static_cast<uint64_t>(ns);
+}
+
 void bl_cluster::refresh_stats() {  // comm_sim.cpp:108-118, 175-180
   cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
   const int latest = static_cast<int>((calls + 1u) & 1u);
@@ -467,6 +492,13 @@ void bl_cluster::check_errors(const std::vector<uint64_t>* off) {
     std::snprintf(buf, sizeof buf, "fused NVLink exchange: rank %llu never signalled (timeout)",
                   e[kErrPeer]);
     fail(BL_ERR_NCCL, buf);
+  }
+  if (e[kErrVerify] != none) {  // comm_sim.cpp:91-101
+    std::snprintf(buf, sizeof buf,
+                  "error-compensation identity violated at element %llu: exceeds relative "
+                  "tolerance %g",
+                  e[kErrVerify], cfg.compensation_tolerance);
+    fail(BL_ERR_LOGIC, buf);
   }
   if (e[kErrRecon] != none) {  // optimizers.cpp:288-293
     std::snprintf(buf, sizeof buf, "non-finite reconstructed gradient for layer 'layer%llu'",
@@ -587,6 +619,7 @@ void bl_optimizer::compressed_step(double lr) {
     p.tile_layer = k1_tile_layer;
     p.slow_list = k1_slow;
     p.n_slow = k1_n_slow;
+    cl->verify_es_one = !hp.scaled_error_feedback;
     cl->compressed(&p, mode, 1.0f, es);
   }
 
@@ -793,11 +826,7 @@ bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
     check_arg(cfg->n_workers >= 1, "SimCluster: need at least one worker");
     check_arg(cfg->dim >= 1, "SimCluster: dim must be >= 1");
     check_arg(cfg->baseline_bits_per_element >= 1, "SimCluster: baseline bits must be >= 1");
-    if (cfg->verify_compensation) {
-      fail(BL_ERR_UNSUPPORTED,
-           "verify_compensation: the fp32 path checks the compensation identity in its test "
-           "suite, not per element at run time");
-    }
+
     if (cfg->n_workers > 64) fail(BL_ERR_UNSUPPORTED, "more than 64 workers");
     if (cfg->mode == BL_MODE_NCCL) {
       check_arg(cfg->rank >= 0 && cfg->rank < cfg->n_workers, "rank out of range");
@@ -936,6 +965,8 @@ bl_status bl_cluster_compressed_allreduce(bl_cluster* c, const float* const* inp
       c->lossless(false);
       c->ledger_compressed();
       c->last_identity = true;
+      if (c->cfg.verify_compensation && error_scale == 1.0)  // v + 0 == v + 0 exactly
+        c->checks += static_cast<uint64_t>(c->nw) * c->n + static_cast<uint64_t>(c->ns);
     } else {
       c->compressed(nullptr, 0, static_cast<float>(error_scale), nullptr);
       const int latest = static_cast<int>((c->calls + 1u) & 1u);
@@ -1083,6 +1114,7 @@ float* bl_cluster_input_buffer(bl_cluster* c, int32_t worker) {
 }
 
 uint64_t bl_cluster_kernel_launches(const bl_cluster* c) { return c ? c->launches : 0; }
+uint64_t bl_cluster_compensation_checks(const bl_cluster* c) { return c ? c->checks : 0; }
 
 bl_status bl_cluster_set_profiling(bl_cluster* c, int32_t on) {
   return guarded([&] {

@@ -93,6 +93,10 @@ struct bl_cluster {
   int* k1_slow = nullptr;       // API-mode K1 tiles that are not full/inside the data
   int k1_n_slow = 0;
 
+  uint64_t checks = 0;          // compensation checks run (comm_sim.hpp:110)
+  bool verify_es_one = true;    // the optimizer's device error scale is 1 (no scaled EF)
+  void verify_last();           // verify_compensation over the local endpoints
+
   uint64_t calls = 0;           // compressed collectives run (ping-pong index)
   bool last_identity = false;
   bl_volume_ledger ledger{};

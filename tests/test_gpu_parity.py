@@ -194,6 +194,18 @@ def test_compensation_identity_and_residual_bound(bl):
     assert mx_d <= 2 * mx_c
 
 
+def test_verify_compensation_counts_and_fails_loudly(bl):
+    """test_comm_sim.cpp:280-289 on the device: n^2 + n checks per call; an
+    fp32 run needs an fp32 tolerance (2^-23), the fp64 default 1e-12 trips."""
+    c = bl.SimCluster(2, 8, verify_compensation=True, compensation_tolerance=2.0 ** -23)
+    for step in range(5):
+        c.compressed_allreduce(rnd((2, 8), 600 + step))
+    assert c.compensation_checks() == 5 * (2 * 2 + 2)
+    tight = bl.SimCluster(1, 2, verify_compensation=True)  # tol 1e-12
+    with pytest.raises(bl.LogicError, match="error-compensation identity violated"):
+        tight.compressed_allreduce(np.array([[1.0, 1e-8]], np.float32))
+
+
 def test_dimension_errors(bl):
     """test_comm_sim.cpp:261-268."""
     c = bl.SimCluster(2, 4)
