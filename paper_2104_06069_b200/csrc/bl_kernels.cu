@@ -250,6 +250,33 @@ __device__ __forceinline__ void flag(unsigned long long* err, int slot, unsigned
   if (err) atomicMin(err + slot, key);
 }
 
+// Tile scheduler.  With a counter, warps take the next tile from it
+// (dynamic: the slowest warp finishes at most one tile after the others
+// instead of a whole grid-stride share); without, the fixed grid-stride
+// sequence.  The counter resets itself: a launch makes exactly
+// total + nwarps fetches and the last one writes 0 back, which stream order
+// makes visible to the next kernel.
+struct TileSched {
+  unsigned int* ctr;
+  long long total, nwarps, cur;
+  __device__ __forceinline__ long long first(long long gw, int lane) {
+    cur = ctr ? fetch(lane) : gw;
+    return cur;
+  }
+  __device__ __forceinline__ long long next(int lane) {
+    cur = ctr ? fetch(lane) : cur + nwarps;
+    return cur;
+  }
+  __device__ __forceinline__ long long fetch(int lane) {
+    unsigned long long v = 0;
+    if (lane == 0) {
+      v = atomicAdd(ctr, 1u);
+      if (static_cast<long long>(v) == total + nwarps - 1) *ctr = 0u;
+    }
+    return static_cast<long long>(__shfl_sync(0xffffffffu, v, 0));
+  }
+};
+
 // ---- fused NVLink exchange: epoch flags in peer memory -----------------------
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
@@ -530,7 +557,8 @@ __global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p
   const long long total = p.slow_list ? static_cast<long long>(p.n_slow) * p.nw : per_w * p.nw;
   const float es = p.es_dev ? __ldg(p.es_dev) : p.es_host;
 
-  for (long long it = gw; it < total; it += nwarps) {
+  TileSched sch{p.slow_list ? nullptr : p.ctr, total, nwarps, 0};
+  for (long long it = sch.first(gw, lane); it < total; it = sch.next(lane)) {
     long long tile = it;
     if (p.slow_list) {  // iterate only the listed boundary tiles of every worker
       const long long wl = it / p.n_slow;
@@ -862,7 +890,8 @@ __global__ void __launch_bounds__(kBlock, NT == 1 ? 4 : (NT == 2 ? 3 : 2)) k3_se
   const double inv_n = 1.0 / static_cast<double>(n);
   if (p.wait_flags) wait_peers(p.wait_flags, n, p.epoch, p.err);
 
-  for (long long tile = gw; tile < total; tile += nwarps) {
+  TileSched sch{p.ctr, total, nwarps, 0};
+  for (long long tile = sch.first(gw, lane); tile < total; tile = sch.next(lane)) {
     const int sv = static_cast<int>(tile / p.tpc);
     const int t = static_cast<int>(tile - static_cast<long long>(sv) * p.tpc);
     const int j = p.server_base + sv;
@@ -1109,7 +1138,8 @@ __global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
   const BitCursor cur{p.res_cur, p.c, p.slot, p.W, p.n};
   const BitCursor prv{p.res_prev, p.c, p.slot, p.W, p.n};
 
-  for (long long tile = gw; tile < p.lt.tiles; tile += nwarps) {
+  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0};
+  for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
     const uint64_t lo = __ldg(p.lt.off + l);
@@ -1308,7 +1338,8 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const BitCursor cur{p.res_cur, p.c, p.slot, p.W, p.n};
-  for (long long tile = gw; tile < p.lt.tiles; tile += nwarps) {
+  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0};
+  for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
     const uint64_t lo = __ldg(p.lt.off + l);
@@ -1385,7 +1416,8 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  for (long long tile = gw; tile < p.lt.tiles; tile += nwarps) {
+  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0};
+  for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
     const uint64_t lo = __ldg(p.lt.off + l);
@@ -1568,7 +1600,8 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  for (long long tile = gw; tile < p.lt.tiles; tile += nwarps) {
+  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0};
+  for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
     const uint64_t lo = __ldg(p.lt.off + l);

@@ -66,6 +66,7 @@ struct K1Params {
   int skip_fast;              // general kernel: leave fast tiles to the bulk kernel
   const int* slow_list;       // general kernel after k1_bulk: the non-fast (j*tpc+t) tiles
   int n_slow;
+  unsigned int* ctr;          // dynamic tile counter (self-resetting) or nullptr
 };
 
 // K3: server reduction of chunk(s) owned locally.
@@ -92,6 +93,7 @@ struct K3Params {
   uint64_t res_off;
   int rank;
   unsigned long long* err;
+  unsigned int* ctr;
 };
 
 struct FinalizeParams {
@@ -121,6 +123,7 @@ struct LayerTiles {
   const uint64_t* off;          // [L+1]
   const int* tile_layer;        // [tiles]
   const int* layer_tile_start;  // [L+1]
+  unsigned int* ctr;            // dynamic tile counter (self-resetting) or nullptr
 };
 
 struct K5Params {

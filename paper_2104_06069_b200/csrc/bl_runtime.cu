@@ -14,6 +14,7 @@
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -167,6 +168,7 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
   p.cmax = cfg.endpoint_stats ? wcmax : nullptr;
   p.err = err;
   p.worker_base = mode == BL_MODE_SIM ? 0 : rank;
+  p.ctr = std::getenv("BL_STATIC_TILES") ? nullptr : tile_ctr;
   const bool p2p = transport == BL_TRANSPORT_P2P;
   const unsigned long long epoch = calls + 1;
   const uint64_t my_slot = (static_cast<uint64_t>(cur()) * n + rank) * slot;
@@ -249,6 +251,7 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
   k3.partials = spart;
   k3.cmax = cfg.endpoint_stats ? scmax : nullptr;
   k3.err = err;
+  k3.ctr = p.ctr;
   if (p2p) {
     k3.peer_res = d_peer_res;  // fused allgather: server words into every peer's result slot
     k3.res_off = my_slot;
@@ -515,6 +518,11 @@ void bl_cluster::sync_and_check(const std::vector<uint64_t>* off) {
 // ---------------------------------------------------------------------------
 // bl_optimizer
 // ---------------------------------------------------------------------------
+bl::LayerTiles bl_optimizer::lt() const {
+  return {L, tiles, off_dev, tile_layer, layer_tile_start,
+          std::getenv("BL_STATIC_TILES") ? nullptr : cl->tile_ctr};
+}
+
 void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, bool adam) {
   // average_lossless (optimizers.cpp:119-138).  With one worker the average
   // (float)((0.0 + g) * 1.0) is g itself: W1 reads the gradient in place and
@@ -876,6 +884,7 @@ bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
       c->spart = dalloc<double>(static_cast<size_t>(c->ns) * c->tpc);
       c->out = dalloc<float>(c->P + kSlack);
       c->err = reinterpret_cast<unsigned long long*>(dalloc<double>(kErrSlots));
+      c->tile_ctr = reinterpret_cast<unsigned int*>(dalloc<float>(4));
       cuda_check(cudaMemset(c->err, 0xFF, kErrSlots * sizeof(unsigned long long)), "err init");
       if (cfg->endpoint_stats) {
         c->wcmax = dalloc<float>(nw * n * c->tpc);
@@ -929,7 +938,7 @@ void bl_cluster_destroy(bl_cluster* c) {
                   c->serr,      c->res_base,   c->wpart,           c->spart,     c->wcmax,
                   c->scmax,     c->out,        c->lrecv,           c->err,       c->stat_part,
                   c->stat_max,  c->stat_out,   c->rx,              c->flags,     c->d_peer_rx,
-                  c->d_peer_res, c->d_peer_flags, c->k1_slow};
+                  c->d_peer_res, c->d_peer_flags, c->k1_slow, c->tile_ctr};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& e : c->pending) {

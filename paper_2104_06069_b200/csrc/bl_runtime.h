@@ -90,6 +90,7 @@ struct bl_cluster {
   std::vector<void*> ipc_opened;
   void setup_p2p(bool required);
 
+  unsigned int* tile_ctr = nullptr;  // dynamic tile counter shared by the stream's kernels
   int* k1_slow = nullptr;       // API-mode K1 tiles that are not full/inside the data
   int k1_n_slow = 0;
 
@@ -164,7 +165,7 @@ struct bl_optimizer {
   bool mprev_separate = false;  // m_prev poked by the caller
   uint64_t my_calls = 0;        // cluster->calls after our last compressed step
 
-  bl::LayerTiles lt() const { return {L, tiles, off_dev, tile_layer, layer_tile_start}; }
+  bl::LayerTiles lt() const;
   bool two_stage() const {
     return variant == BL_ONEBIT_LAMB || variant == BL_LAMB_BASIC_ONEBIT || variant == BL_ONEBIT_ADAM;
   }
