@@ -691,19 +691,35 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
                p.res_prev + static_cast<size_t>(j) * p.slot + (i0 >> 5) + 4 * r0, kBulkBits, bar);
   };
 
-  long long ptile = next_fast(gw);
+  // Producer sequence: with a tile counter the fast tiles are taken
+  // dynamically (boundary tiles are skipped here and done below from the
+  // slow list); each issued batch records its (tile, r0) in the stage slot
+  // so the consumer replays exactly the producer's order.
+  __shared__ long long s_tile[kBulkWarps][kBulkStages];
+  __shared__ int s_r0[kBulkWarps][kBulkStages];
+  TileSched sch{p.ctr, total, nwarps, 0};
+  auto fetch_fast = [&](bool first) {
+    long long t = first ? sch.first(gw, lane) : sch.next(lane);
+    while (t < total && !is_fast(t)) t = sch.next(lane);
+    return t;
+  };
+  long long ptile = p.ctr ? fetch_fast(true) : next_fast(gw);
   int pr = 0;
-  auto advance = [&](long long& tile, int& r0) {
-    r0 += kBulkR;
-    if (r0 == kRowsPerTile) {
-      r0 = 0;
-      tile = next_fast(tile + nwarps);
+  auto produce = [&](int stage) {
+    if (lane == 0) {
+      s_tile[wib][stage] = ptile;
+      s_r0[wib][stage] = pr;
+    }
+    issue(stage, ptile, pr);
+    if (ptile >= total) return;
+    pr += kBulkR;
+    if (pr == kRowsPerTile) {
+      pr = 0;
+      ptile = p.ctr ? fetch_fast(false) : next_fast(ptile + nwarps);
     }
   };
-  for (int s = 0; s < kBulkStages; ++s) {
-    issue(s, ptile, pr);
-    advance(ptile, pr);
-  }
+  for (int s = 0; s < kBulkStages; ++s) produce(s);
+  __syncwarp();
   // Boundary tiles (layer boundaries, chunk/padding ends) take the general
   // path here, while the prologue copies are in flight.
   if (p.slow_list) {
@@ -714,7 +730,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
     }
   }
 
-  long long ctile = next_fast(gw);
+  long long ctile = 0;
   int cr = 0;
   uint32_t b = 0;
   // per-tile consumer state
@@ -731,9 +747,12 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
   const bool stats = p.cmax != nullptr;
   const uint32_t sh = 4 * (lane & 7);
   const int wsub = lane >> 3;
-  while (ctile < total) {
+  while (true) {
     const int stage = static_cast<int>(b % kBulkStages);
     const uint32_t phase = (b / kBulkStages) & 1u;
+    ctile = s_tile[wib][stage];
+    cr = s_r0[wib][stage];
+    if (ctile >= total) break;
     if (cr == 0) {
       w = static_cast<int>(ctile / per_w);
       const long long rem = ctile - w * per_w;
@@ -807,8 +826,8 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
       stage_row_bits(sw, cr + k, lane, nib);
     }
     __syncwarp();  // every lane is done with this stage before it is refilled
-    issue(stage, ptile, pr);
-    advance(ptile, pr);
+    produce(stage);
+    __syncwarp();
     if (cr + kBulkR == kRowsPerTile) {
       const uint4 wv = tile_words(sw, lane);
       reinterpret_cast<uint4*>(pkc)[lane] = wv;
@@ -820,7 +839,6 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
         if (lane == 0) p.cmax[ep * p.tpc + t] = m;
       }
     }
-    advance(ctile, cr);
     ++b;
   }
   if (p.peer_rx) warp_fence_system(lane);
@@ -1924,7 +1942,10 @@ static bool bulk_none() {
 }
 
 bool k1_uses_bulk(const K1Params& p, int mode) {
-  const bool misaligned = (p.c & 3u) != 0;
+  // Only odd chunk lengths (4-byte-aligned chunk starts) go through the bulk
+  // pipeline; 8-byte-aligned chunks load as float2 on the register path,
+  // which measures faster there (BERT-L sim2: 1.35 vs 1.42 ms).
+  const bool misaligned = (p.c & 1u) != 0;
   return mode != 1 && (mode == 0 || p.tile_layer) && (misaligned || bulk_all()) && !bulk_none();
 }
 
@@ -1941,9 +1962,9 @@ int launch_k1_phase(const K1Params& p, int mode, int phase, cudaStream_t s) {
 
 int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
   if (k1_uses_bulk(p, mode)) {
-    // Misaligned chunks: fast tiles through the bulk-copy pipeline (g staged
-    // with alignment slack), then the boundary tiles through the general
-    // kernel.  Aligned chunks stay on the register path, which measures faster.
+    // Odd chunks: fast tiles through the bulk-copy pipeline (g staged with
+    // alignment slack); the boundary tiles run in the same kernel from the
+    // slow list.  Aligned chunks stay on the register path.
     return launch_k1_phase(p, mode, 0, s);
   }
   K1Params full = p;  // register path: every tile, the slow list does not apply
