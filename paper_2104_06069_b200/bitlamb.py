@@ -17,7 +17,8 @@ from typing import Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbitlamb_b200.so")
+# BL_LIB_PATH: an alternative build of the same library (A/B timing).
+LIB_PATH = os.environ.get("BL_LIB_PATH") or os.path.join(_HERE, "libbitlamb_b200.so")
 
 # ---------------------------------------------------------------------------
 # Exceptions: errors.hpp:26-53 (bl_status codes 1..6) + CUDA/NCCL/unsupported.
