@@ -110,6 +110,8 @@ class SimCluster {
     CompressorKind compressor = CompressorKind::kOneBit;
     int baseline_bits_per_element = 16;
     bool endpoint_stats = false;
+    bool verify_compensation = false;       // comm_sim.hpp:78
+    double compensation_tolerance = 1e-12;  // fp32 state needs >= 2^-23
     int device = 0;
     void* stream = nullptr;
     bl_transport transport = BL_TRANSPORT_AUTO;  // NCCL mode: fused NVLink or NCCL
@@ -191,6 +193,22 @@ class SimCluster {
     check(bl_cluster_stats(h_, s.data()));
     return s;
   }
+  // comm_sim.hpp:113-124: endpoint statistics (workers, then chunk servers)
+  // and their maxima; needs Config::endpoint_stats.
+  std::vector<EndpointStats> worker_stats() const {
+    auto s = stats();
+    return {s.begin(), s.begin() + n_};
+  }
+  std::vector<EndpointStats> server_stats() const {
+    auto s = stats();
+    return {s.begin() + n_, s.end()};
+  }
+  double delta_linf() const { return max_of(&EndpointStats::delta_linf); }
+  double delta_l2_max() const { return max_of(&EndpointStats::delta_l2); }
+  double run_max_delta_linf() const { return max_of(&EndpointStats::max_delta_linf); }
+  double run_max_corrected_linf() const { return max_of(&EndpointStats::max_corrected_linf); }
+  std::uint64_t compensation_checks() const { return bl_cluster_compensation_checks(h_); }
+
   int n_workers() const { return n_; }
   std::size_t dim() const { return dim_; }
   std::size_t padded() const { return padded_; }
@@ -199,6 +217,11 @@ class SimCluster {
   bl_cluster* handle() const { return h_; }
 
  private:
+  double max_of(double EndpointStats::*field) const {
+    double m = 0.0;
+    for (const auto& e : stats()) m = m < e.*field ? e.*field : m;
+    return m;
+  }
   static bl_cluster_config base(const Config& cfg) {
     bl_cluster_config c{};
     c.n_workers = cfg.n_workers;
@@ -207,7 +230,8 @@ class SimCluster {
     c.compressor = static_cast<int32_t>(cfg.compressor);
     c.baseline_bits_per_element = cfg.baseline_bits_per_element;
     c.endpoint_stats = cfg.endpoint_stats ? 1 : 0;
-    c.compensation_tolerance = 1e-12;
+    c.verify_compensation = cfg.verify_compensation ? 1 : 0;
+    c.compensation_tolerance = cfg.compensation_tolerance;
     c.stream = cfg.stream;
     c.transport = cfg.transport;
     return c;
