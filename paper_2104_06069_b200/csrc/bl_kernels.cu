@@ -846,12 +846,29 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
 
 // Scale of each endpoint: S = (float)(sum|corrected| / c) (compression.cpp:54-55),
 // non-finite -> flag (compression.cpp:56-58).  One 1024-thread block per endpoint.
+// s = a[t0] + a[t0 + step] + ... (t < t1), added in that order from 0; the
+// loads are issued 8 at a time so the dependent fp64 adds do not wait on
+// one load each (the canonical stripe sums of finalize / epilogues).
+template <int STEP = 1024>
+__device__ __forceinline__ double stripe_sum(const double* a, long long t0, long long t1) {
+  double s = 0.0;
+  long long t = t0;
+  for (; t + 7ll * STEP < t1; t += 8ll * STEP) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = a[t + k * STEP];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  for (; t < t1; t += STEP) s += a[t];
+  return s;
+}
+
 __global__ void __launch_bounds__(1024) k_finalize_scales(const FinalizeParams p) {
   __shared__ double sh[32];
   const int e = blockIdx.x;
   const double* part = p.partials + static_cast<size_t>(e) * p.tpc;
-  double s = 0.0;
-  for (int t = threadIdx.x; t < p.tpc; t += 1024) s += part[t];
+  double s = stripe_sum(part, threadIdx.x, p.tpc);
   s = block1024_sum(s, sh);
   if (threadIdx.x == 0) {
     const float S = static_cast<float>(s / static_cast<double>(p.c));
@@ -1301,10 +1318,9 @@ __global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
   __shared__ bool last;
   const int l = blockIdx.x;
   const int t0 = p.layer_tile_start[l], t1 = p.layer_tile_start[l + 1];
-  double s = 0.0;
+  double s = stripe_sum(p.tile_v2, t0 + threadIdx.x, t1);
   float mx = 0.0f;
   for (int t = t0 + threadIdx.x; t < t1; t += 1024) {
-    s += p.tile_v2[t];
     const float m = p.tile_max[t];
     mx = mx < m ? m : mx;
   }
@@ -1338,9 +1354,16 @@ __global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
   __syncthreads();
   if (last && threadIdx.x == 0) {
     __threadfence();
-    const volatile double* tr = p.trace;
-    double c_sum = 0.0;
-    for (int k = 0; k < p.L; ++k) c_sum += tr[k];
+    double c_sum = 0.0;  // ascending over layers; L2 loads, 8 in flight
+    int k = 0;
+    for (; k + 8 <= p.L; k += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldcg(p.trace + k + q);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c_sum += v[q];
+    }
+    for (; k < p.L; ++k) c_sum += __ldcg(p.trace + k);
     p.cmean[1] = p.cmean[0];
     const double cm = c_sum / static_cast<double>(p.L);
     p.cmean[0] = cm < p.floor_ ? p.floor_ : cm;
@@ -1542,13 +1565,11 @@ __global__ void __launch_bounds__(1024) k_wepilogue(const WEpiParams p) {
   __shared__ bool last;
   const int l = blockIdx.x;
   const int t0 = p.layer_tile_start[l], t1 = p.layer_tile_start[l + 1];
-  double sx = 0.0, su = 0.0, sv = 0.0, sm = 0.0;
-  for (int t = t0 + threadIdx.x; t < t1; t += 1024) {
-    sx += p.tile_sums[4 * t + 0];
-    su += p.tile_sums[4 * t + 1];
-    sv += p.tile_sums[4 * t + 2];
-    sm += p.tile_sums[4 * t + 3];
-  }
+  const long long a0 = 4ll * (t0 + threadIdx.x), a1 = 4ll * t1;
+  double sx = stripe_sum<4096>(p.tile_sums + 0, a0, a1);
+  double su = stripe_sum<4096>(p.tile_sums + 1, a0, a1);
+  double sv = stripe_sum<4096>(p.tile_sums + 2, a0, a1);
+  double sm = stripe_sum<4096>(p.tile_sums + 3, a0, a1);
   sx = block1024_sum(sx, shd);
   su = block1024_sum(su, shd);
   sv = block1024_sum(sv, shd);
