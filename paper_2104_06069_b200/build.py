@@ -49,8 +49,9 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """Build the library; `out`/`defines` make A/B variants (-D tuning knobs)."""
+    if out == OUT and not defines and not force and not needs_build():
         return OUT
     inc, lib = nccl_dirs()
     host_cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
@@ -58,13 +59,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-shared", f"-I{inc}",
            *[os.path.join(CSRC, s) for s in SOURCES],
            f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-lcudart",
-           "-o", OUT + ".tmp"]
+           *defines, "-o", out + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True, cwd=CSRC)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--out PATH -DKNOB=V ...]  (variants for A/B timing)
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else OUT
+    defs = [a for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=os.path.abspath(out), defines=defs))

@@ -902,8 +902,28 @@ __device__ __forceinline__ void flush_server_words(const K3Params& p, uint32_t* 
   }
 }
 
+#ifndef K3_R1
+#define K3_R1 8
+#endif
+#ifndef K3_R2
+#define K3_R2 4
+#endif
+#ifndef K3_R4
+#define K3_R4 4
+#endif
+#ifndef K3_B4
+#define K3_B4 3
+#endif
+#ifndef K3_B8
+#define K3_B8 2
+#endif
+#ifndef K3_B2
+#define K3_B2 3
+#endif
+#define K3_ROWS(NT) ((NT) == 1 ? K3_R1 : (NT) == 2 ? K3_R2 : (NT) == 4 ? K3_R4 : 4)
+#define K3_MINB(NT) ((NT) == 1 ? (K3_R1 == 8 ? 3 : 4) : (NT) == 2 ? K3_B2 : (NT) == 4 ? K3_B4 : (NT) == 8 ? K3_B8 : 2)
 template <int NT>
-__global__ void __launch_bounds__(kBlock, NT == 1 ? 4 : (NT == 2 ? 3 : 2)) k3_server_reduce(const K3Params p) {
+__global__ void __launch_bounds__(kBlock, K3_MINB(NT)) k3_server_reduce(const K3Params p) {
   __shared__ float s_scale[kWarpsPerBlock][64];
   __shared__ uint32_t* s_peer[64];
   __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
@@ -943,8 +963,10 @@ __global__ void __launch_bounds__(kBlock, NT == 1 ? 4 : (NT == 2 ? 3 : 2)) k3_se
     const uint32_t* inw = in + (i0 >> 5);
 
     if (NT > 0 && i0 + kTile <= p.c) {
-      // Fast path: full tile, 4 rows per batch with every load issued first.
-      constexpr int R = 4;
+      // Fast path: full tile, R rows per batch with every load issued first.
+      // One streamed array (serr): small n takes 8 rows per batch to keep
+      // as many bytes in flight as the two-array kernels.
+      constexpr int R = K3_ROWS(NT);
       const uint32_t sh = 4 * (lane & 7);
       const int wsub = lane >> 3;
       const bool stats = p.cmax != nullptr;
