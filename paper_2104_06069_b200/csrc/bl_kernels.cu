@@ -323,6 +323,12 @@ __device__ __forceinline__ void wait_peers(const unsigned long long* flags, int 
 // ---------------------------------------------------------------------------
 // One K1 tile (general path: any alignment, layer boundaries, padding, partial
 // tiles).  The per-warp word buffer `sw` stages the tile's packet words.
+#ifndef K1_ROWS
+#define K1_ROWS 8  // rows per load batch in K1's register path
+#endif
+#ifndef K1_MINB
+#define K1_MINB 2  // resident CTAs per SM requested from ptxas
+#endif
 template <int MODE, bool ALIGNED>
 __device__ __forceinline__ void k1_tile(const K1Params& p, long long tile, int lane, uint32_t* sw,
                                         float es) {
@@ -376,7 +382,7 @@ __device__ __forceinline__ void k1_tile(const K1Params& p, long long tile, int l
   }
   if (fast && p.skip_fast) return;  // done by k1_bulk
   if (fast) {
-    constexpr int R = 4;
+    constexpr int R = K1_ROWS;
     const uint32_t sh = 4 * (lane & 7);
     const int wsub = lane >> 3;
     const bool stats = p.cmax != nullptr;
@@ -547,7 +553,7 @@ __device__ __forceinline__ void k1_tile(const K1Params& p, long long tile, int l
 }
 
 template <int MODE, bool ALIGNED>
-__global__ void __launch_bounds__(kBlock, 3) k1_worker_compress(const K1Params p) {
+__global__ void __launch_bounds__(kBlock, K1_MINB) k1_worker_compress(const K1Params p) {
   __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
   uint32_t* sw = s_words[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1186,8 +1192,14 @@ __device__ __forceinline__ int lane_valid(uint64_t len, uint64_t ir, int lane) {
 // MPREV 0: m_prev from the momentum buffer (first step after the freeze);
 // MPREV 1: m_prev from the previous result packets.
 // ---------------------------------------------------------------------------
+#ifndef K5_ROWS
+#define K5_ROWS 4
+#endif
+#ifndef K5_MINB
+#define K5_MINB 3
+#endif
 template <int MPREV>
-__global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
+__global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p) {
   if (p.wait_flags) wait_peers(p.wait_flags, p.n, p.epoch, p.err);
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1210,7 +1222,7 @@ __global__ void __launch_bounds__(kBlock) k5_update_a(const K5Params p) {
     if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce && !p.dense &&
         !p.norm_only) {
       // Fast path: aligned, full tile, one chunk of the result.
-      constexpr int R = 4;
+      constexpr int R = K5_ROWS;
       const uint32_t* sl = cur.res + j * p.slot;
       const float S = slot_scale_cg(sl, p.W);
       const float pos = S, neg = S == 0.0f ? 0.0f : -S;
