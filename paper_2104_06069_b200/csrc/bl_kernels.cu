@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -1783,6 +1784,108 @@ __global__ void k_average(const float* in, uint64_t stride, int n, uint64_t len,
   }
 }
 
+// Lossless all-reduce over NVLink (comm_sim.cpp:205-232 in P2P mode): rank r
+// reads chunk r of every rank's gradient straight from the peers' HBM,
+// averages it in ascending rank order in fp64 (x 1/n, the k_average
+// arithmetic), and stores the result into every rank's output — the
+// reduce-scatter and the allgather in one pass, no staging copy.  The
+// finite check of check_gradients (optimizers.cpp:99-117) rides along: a
+// non-finite element of rank q is reported into rank q's own error word.
+// U groups of 4 elements (k0, k0 + step, ...) per thread: all peers' loads
+// of all groups are issued before any is consumed (NVLink latency).
+template <int NT, int U>
+__device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint64_t k0,
+                                                uint64_t step, uint64_t end, double inv_n) {
+  constexpr int kN = NT > 0 ? NT : 8;
+  const int n = NT > 0 ? NT : p.n;
+  float4 g[U][kN];
+  double a[U][4];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) a[u][e] = 0.0;
+  for (int q0 = 0; q0 < n; q0 += kN) {
+    const int m = n - q0 < kN ? n - q0 : kN;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t k = k0 + u * step;
+#pragma unroll
+      for (int q = 0; q < kN; ++q)
+        if (q < m && k < end) g[u][q] = __ldcg(reinterpret_cast<const float4*>(p.peer_in[q0 + q] + k));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t k = k0 + u * step;
+      if (k >= end) break;
+#pragma unroll
+      for (int q = 0; q < kN; ++q) {
+        if (q >= m) break;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float x = comp(g[u][q], e);
+          if (p.check_finite && !isfinite(x) && k + e < p.d)
+            atomicMin_system(p.peer_err[q0 + q] + kErrGrad,
+                             (static_cast<unsigned long long>(q0 + q) << 40) | (k + e));
+          a[u][e] += static_cast<double>(x);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t k = k0 + u * step;
+    if (k >= end) break;
+    const float4 v = make_float4(static_cast<float>(a[u][0] * inv_n), static_cast<float>(a[u][1] * inv_n),
+                                 static_cast<float>(a[u][2] * inv_n), static_cast<float>(a[u][3] * inv_n));
+    for (int q = 0; q < n; ++q) *reinterpret_cast<float4*>(p.peer_out[q] + k) = v;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p) {
+  wait_peers(p.in_flags, p.n, p.epoch, p.err);  // every rank's gradient is in place
+  const double inv_n = 1.0 / static_cast<double>(p.n);
+  const uint64_t lo = static_cast<uint64_t>(p.rank) * p.c, hi = lo + p.c;
+  const uint64_t up = (lo + 3) & ~3ull, dn = hi & ~3ull;  // 16-B aligned body [a0, a1)
+  const uint64_t a0 = up < hi ? up : hi;
+  const uint64_t a1 = dn > a0 ? dn : a0;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  constexpr int U = NT == 8 ? 1 : 2;
+  for (uint64_t k = a0 + 4 * tid; k < a1; k += 4 * nth * U)
+    lossless_groups<NT, U>(p, k, 4 * nth, a1, inv_n);
+  if (blockIdx.x == 0) {  // unaligned head [lo, a0) and tail [a1, hi), one element per thread
+    const uint64_t nh = a0 - lo, nt = hi - a1;
+    if (threadIdx.x < nh + nt) {
+      const uint64_t k = threadIdx.x < nh ? lo + threadIdx.x : a1 + (threadIdx.x - nh);
+      double acc = 0.0;
+      for (int q = 0; q < p.n; ++q) {
+        const float x = __ldcg(p.peer_in[q] + k);
+        if (p.check_finite && !isfinite(x) && k < p.d)
+          atomicMin_system(p.peer_err[q] + kErrGrad, (static_cast<unsigned long long>(q) << 40) | k);
+        acc += static_cast<double>(x);
+      }
+      const float v = static_cast<float>(acc * inv_n);
+      for (int q = 0; q < p.n; ++q) p.peer_out[q][k] = v;
+    }
+  }
+  __threadfence_system();  // this thread's remote stores and error reports
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(p.done, 1u) == gridDim.x - 1) {
+    *p.done = 0u;
+    __threadfence_system();
+    for (int q = 0; q < p.n; ++q) st_release_sys(p.peer_flags[q] + p.out_flag + p.rank, p.epoch);
+  }
+}
+
+__global__ void k_signal_peers(unsigned long long* const* peer_flags, int index, int n,
+                               unsigned long long epoch) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < n; ++q) st_release_sys(peer_flags[q] + index, epoch);
+  }
+}
+
 // Result of the collective (compression.cpp:68-81, comm_sim.cpp:173,202):
 // chunk-relative, one warp per 32 packet words (1024 elements): every lane
 // reads the same word (broadcast) and writes one element of each 32-element
@@ -2130,6 +2233,24 @@ int launch_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const fl
                         const uint64_t* off, int L, const float* A, const float* B,
                         unsigned long long* err, int worker_base, cudaStream_t s) {
   k_build_stream<<<grid_for_elems(d), 256, 0, s>>>(in, stride, nw, d, m, off, L, A, B, err, worker_base);
+  return 1;
+}
+
+int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s) {
+  const long long groups = static_cast<long long>(p.c / 4) + 1;
+  const int want = static_cast<int>(std::min<long long>((groups + 255) / 256, 8ll * sms));
+  switch (p.n) {
+    case 2: k_lossless_p2p<2><<<resident(k_lossless_p2p<2>, want), 256, 0, s>>>(p); break;
+    case 4: k_lossless_p2p<4><<<resident(k_lossless_p2p<4>, want), 256, 0, s>>>(p); break;
+    case 8: k_lossless_p2p<8><<<resident(k_lossless_p2p<8>, want), 256, 0, s>>>(p); break;
+    default: k_lossless_p2p<0><<<resident(k_lossless_p2p<0>, want), 256, 0, s>>>(p); break;
+  }
+  return 1;
+}
+
+int launch_signal_peers(unsigned long long* const* peer_flags, int index, int n,
+                        unsigned long long epoch, cudaStream_t s) {
+  k_signal_peers<<<1, 32, 0, s>>>(peer_flags, index, n, epoch);
   return 1;
 }
 

@@ -177,6 +177,21 @@ struct K6Params {
   const float* dense;  // identity compressor: dense result
 };
 
+// Deterministic lossless all-reduce over NVLink peer memory (P2P transport).
+struct LosslessP2PParams {
+  const float* const* peer_in;            // [n] every rank's gradient buffer
+  float* const* peer_out;                 // [n] every rank's output buffer
+  unsigned long long* const* peer_err;    // [n] every rank's error words
+  unsigned long long* const* peer_flags;  // [n] every rank's flag words
+  const unsigned long long* in_flags;     // local [n]: rank q's gradient is in place
+  int out_flag;                           // flag index of "rank's chunk delivered" (+ rank)
+  int n, rank, check_finite;
+  uint64_t c, d;
+  unsigned long long epoch;
+  unsigned int* done;                     // local CTA counter (self-resetting)
+  unsigned long long* err;
+};
+
 struct W1Params {
   LayerTiles lt;
   const float* gbar;
@@ -256,6 +271,11 @@ int launch_set_float(float* p, float v, cudaStream_t s);
 int launch_verify(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot, uint64_t W,
                   uint64_t c, uint64_t len, double tol, unsigned long long* err, cudaStream_t s);
 // Block the stream until flags[0..n) >= epoch (peer signals, bounded wait).
+int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s);
+// Raise flag `index` (+ own rank) at every peer to `epoch` after this stream's
+// prior work (system-scope release).
+int launch_signal_peers(unsigned long long* const* peer_flags, int index, int n,
+                        unsigned long long epoch, cudaStream_t s);
 int launch_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
                       unsigned long long* err, cudaStream_t s);
 // Identity-compressor stream build in place (optimizers.cpp:248-255):

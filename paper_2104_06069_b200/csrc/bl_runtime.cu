@@ -297,47 +297,46 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
 void bl_cluster::setup_p2p(bool required) {
   const size_t nn = static_cast<size_t>(n);
   rx = dalloc<uint32_t>(2 * nn * slot);
-  flags = reinterpret_cast<unsigned long long*>(dalloc<double>(2 * nn));
+  flags = reinterpret_cast<unsigned long long*>(dalloc<double>(4 * nn));
+  lossless_done = reinterpret_cast<unsigned int*>(dalloc<float>(1));
+  // Buffers every peer maps: packet receive slots, result packets, flags,
+  // gradient (lossless reads), output (lossless allgather), error words.
+  constexpr int kB = 6;
+  void* const local[kB] = {rx, res_base, flags, in, out, err};
   constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
-  std::vector<uint8_t> mine(3 * kH);
-  cudaIpcMemHandle_t h[3];
-  cuda_check(cudaIpcGetMemHandle(&h[0], rx), "cudaIpcGetMemHandle(rx)");
-  cuda_check(cudaIpcGetMemHandle(&h[1], res_base), "cudaIpcGetMemHandle(res)");
-  cuda_check(cudaIpcGetMemHandle(&h[2], flags), "cudaIpcGetMemHandle(flags)");
-  std::memcpy(mine.data(), h, 3 * kH);
-  uint8_t* dbuf = reinterpret_cast<uint8_t*>(dalloc<double>((nn * 3 * kH + 7) / 8 + 1));
-  cuda_check(cudaMemcpy(dbuf + static_cast<size_t>(rank) * 3 * kH, mine.data(), 3 * kH,
+  std::vector<uint8_t> mine(kB * kH);
+  for (int k = 0; k < kB; ++k) {
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, local[k]), "cudaIpcGetMemHandle");
+    std::memcpy(mine.data() + k * kH, &h, kH);
+  }
+  uint8_t* dbuf = reinterpret_cast<uint8_t*>(dalloc<double>((nn * kB * kH + 7) / 8 + 1));
+  cuda_check(cudaMemcpy(dbuf + static_cast<size_t>(rank) * kB * kH, mine.data(), kB * kH,
                         cudaMemcpyHostToDevice),
              "handle upload");
-  nccl_check(ncclAllGather(dbuf + static_cast<size_t>(rank) * 3 * kH, dbuf, 3 * kH, ncclUint8, comm,
+  nccl_check(ncclAllGather(dbuf + static_cast<size_t>(rank) * kB * kH, dbuf, kB * kH, ncclUint8, comm,
                            stream),
              "ncclAllGather(handles)");
-  std::vector<uint8_t> all(nn * 3 * kH);
+  std::vector<uint8_t> all(nn * kB * kH);
   cuda_check(cudaMemcpyAsync(all.data(), dbuf, all.size(), cudaMemcpyDeviceToHost, stream), "handles");
   cuda_check(cudaStreamSynchronize(stream), "handles sync");
-  std::vector<void*> prx(nn), pres(nn), pfl(nn);
+  std::vector<std::vector<void*>> peer(kB, std::vector<void*>(nn, nullptr));
   int ok = 1;
   for (int q = 0; q < n; ++q) {
-    if (q == rank) {
-      prx[q] = rx;
-      pres[q] = res_base;
-      pfl[q] = flags;
-      continue;
-    }
-    void* ptrs[3] = {nullptr, nullptr, nullptr};
-    for (int k = 0; k < 3 && ok; ++k) {
+    for (int k = 0; k < kB && ok; ++k) {
+      if (q == rank) {
+        peer[k][q] = local[k];
+        continue;
+      }
       cudaIpcMemHandle_t hq;
-      std::memcpy(&hq, all.data() + (static_cast<size_t>(q) * 3 + k) * kH, kH);
-      if (cudaIpcOpenMemHandle(&ptrs[k], hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      std::memcpy(&hq, all.data() + (static_cast<size_t>(q) * kB + k) * kH, kH);
+      if (cudaIpcOpenMemHandle(&peer[k][q], hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
         cudaGetLastError();
         ok = 0;
       } else {
-        ipc_opened.push_back(ptrs[k]);
+        ipc_opened.push_back(peer[k][q]);
       }
     }
-    prx[q] = ptrs[0];
-    pres[q] = ptrs[1];
-    pfl[q] = ptrs[2];
   }
   int* dok = reinterpret_cast<int*>(dbuf);
   cuda_check(cudaMemcpy(dok, &ok, sizeof ok, cudaMemcpyHostToDevice), "ok upload");
@@ -352,12 +351,17 @@ void bl_cluster::setup_p2p(bool required) {
     transport = BL_TRANSPORT_NCCL;
     return;
   }
-  d_peer_rx = reinterpret_cast<uint32_t**>(dalloc<double>(nn));
-  d_peer_res = reinterpret_cast<uint32_t**>(dalloc<double>(nn));
-  d_peer_flags = reinterpret_cast<unsigned long long**>(dalloc<double>(nn));
-  cuda_check(cudaMemcpy(d_peer_rx, prx.data(), nn * sizeof(void*), cudaMemcpyHostToDevice), "tables");
-  cuda_check(cudaMemcpy(d_peer_res, pres.data(), nn * sizeof(void*), cudaMemcpyHostToDevice), "tables");
-  cuda_check(cudaMemcpy(d_peer_flags, pfl.data(), nn * sizeof(void*), cudaMemcpyHostToDevice), "tables");
+  auto table = [&](int k) {
+    void** t = reinterpret_cast<void**>(dalloc<double>(nn));
+    cuda_check(cudaMemcpy(t, peer[k].data(), nn * sizeof(void*), cudaMemcpyHostToDevice), "tables");
+    return t;
+  };
+  d_peer_rx = reinterpret_cast<uint32_t**>(table(0));
+  d_peer_res = reinterpret_cast<uint32_t**>(table(1));
+  d_peer_flags = reinterpret_cast<unsigned long long**>(table(2));
+  d_peer_in = reinterpret_cast<float**>(table(3));
+  d_peer_out = reinterpret_cast<float**>(table(4));
+  d_peer_err = reinterpret_cast<unsigned long long**>(table(5));
   transport = BL_TRANSPORT_P2P;
 }
 
@@ -369,8 +373,38 @@ void bl_cluster::lossless(bool check_finite) {
                                   mode == BL_MODE_SIM ? 0 : rank, stream));
     return;
   }
+  if (transport == BL_TRANSPORT_P2P) {
+    // One kernel over NVLink peer memory: flag "my gradient is in place" to
+    // every peer, average chunk `rank` from all peers' buffers (reads) into
+    // every peer's output (stores), then wait for every rank's chunk.
+    const unsigned long long ep = ++lcalls;
+    const int nn = n;
+    begin(KC_A2A, &a);
+    end(KC_A2A, a, launch_signal_peers(d_peer_flags, 2 * nn + rank, nn, ep, stream));
+    LosslessP2PParams lp{};
+    lp.peer_in = d_peer_in;
+    lp.peer_out = d_peer_out;
+    lp.peer_err = d_peer_err;
+    lp.peer_flags = d_peer_flags;
+    lp.in_flags = flags + 2 * nn;
+    lp.out_flag = 3 * nn;
+    lp.n = nn;
+    lp.rank = rank;
+    lp.check_finite = check_finite ? 1 : 0;
+    lp.c = c;
+    lp.d = dim;
+    lp.epoch = ep;
+    lp.done = lossless_done;
+    lp.err = err;
+    begin(KC_AVG, &a);
+    end(KC_AVG, a, launch_lossless_p2p(lp, sms, stream));
+    begin(KC_AG, &a);
+    end(KC_AG, a, launch_wait_peers(flags + 3 * nn, nn, ep, err, stream));
+    return;
+  }
   // Deterministic all-reduce: alltoall of fp32 chunks, ascending-rank fp64
   // average of the own chunk, allgather (same bytes as a ring RS + AG).
+  if (!lrecv) lrecv = dalloc<float>(static_cast<size_t>(n) * c_pad + kSlack);
   begin(KC_A2A, &a);
   cuda_check(cudaMemcpyAsync(lrecv + static_cast<size_t>(rank) * c_pad,
                              in + static_cast<size_t>(rank) * c, c * sizeof(float),
@@ -911,7 +945,6 @@ bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
       }
       if (c->mode == BL_MODE_NCCL) {
         c->rpk = dalloc<uint32_t>(n * c->slot);
-        c->lrecv = dalloc<float>(n * c->c_pad + kSlack);
         ncclUniqueId id;
         std::memcpy(id.internal, cfg->nccl_unique_id, BL_NCCL_UNIQUE_ID_BYTES);
         nccl_check(ncclCommInitRank(&c->comm, c->n, id, c->rank), "ncclCommInitRank");
@@ -938,7 +971,8 @@ void bl_cluster_destroy(bl_cluster* c) {
                   c->serr,      c->res_base,   c->wpart,           c->spart,     c->wcmax,
                   c->scmax,     c->out,        c->lrecv,           c->err,       c->stat_part,
                   c->stat_max,  c->stat_out,   c->rx,              c->flags,     c->d_peer_rx,
-                  c->d_peer_res, c->d_peer_flags, c->k1_slow, c->tile_ctr};
+                  c->d_peer_res, c->d_peer_flags, c->d_peer_in, c->d_peer_out, c->d_peer_err,
+                  c->lossless_done, c->k1_slow, c->tile_ctr};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& e : c->pending) {

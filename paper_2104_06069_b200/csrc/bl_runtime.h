@@ -83,10 +83,17 @@ struct bl_cluster {
   int transport = BL_TRANSPORT_NCCL;
   uint32_t* res_base = nullptr;       // one allocation: res[0] | res[1]
   uint32_t* rx = nullptr;             // [2][n][slot] worker packets addressed to this rank
-  unsigned long long* flags = nullptr;  // [2n]: worker-packet flags, server-packet flags
+  // [4n] flags, one per sending rank: worker packets, server packets,
+  // lossless input in place, lossless chunk delivered
+  unsigned long long* flags = nullptr;
   uint32_t** d_peer_rx = nullptr;     // [n] device table of peers' rx
   uint32_t** d_peer_res = nullptr;    // [n] device table of peers' res_base
   unsigned long long** d_peer_flags = nullptr;  // [n]
+  float** d_peer_in = nullptr;        // [n] peers' gradient buffers (lossless over NVLink)
+  float** d_peer_out = nullptr;       // [n] peers' output buffers
+  unsigned long long** d_peer_err = nullptr;  // [n] peers' error words
+  unsigned int* lossless_done = nullptr;
+  unsigned long long lcalls = 0;      // lossless collectives run (flag epoch)
   std::vector<void*> ipc_opened;
   void setup_p2p(bool required);
 

@@ -78,11 +78,13 @@ def main() -> int:
         led = cl.ledger()
         if rank == 0:
             check(led == sim.ledger(), f"d={d} ledger")
-        lo = cl.lossless_allreduce(x[rank])
-        los = gather_bytes(lo.tobytes())
-        if rank == 0:
-            ref = sim.lossless_allreduce(x)
-            check(all(b == ref.tobytes() for b in los), f"d={d} lossless")
+        for rep in range(3):  # several epochs of the lossless exchange
+            x = rng.standard_normal((world, d)).astype(np.float32)
+            lo = cl.lossless_allreduce(x[rank])
+            los = gather_bytes(lo.tobytes())
+            if rank == 0:
+                ref = sim.lossless_allreduce(x)
+                check(all(b == ref.tobytes() for b in los), f"{tp} d={d} lossless rep {rep}")
         cl.close()
         if sim:
             sim.close()
@@ -138,6 +140,30 @@ def optimizer_check(rank, world, local, new_uid, check, tp):
         if rank == 0:
             ref = sopt.get(k).tobytes()
             check(all(v == ref for v in vals), f"{tp} optimizer {k}")
+    opt.close()
+    cl.close()
+
+    # check_gradients (optimizers.cpp:99-117) in the multi-process warmup: a
+    # non-finite element of the last rank's gradient lying in chunk 0 is read
+    # by rank 0 (over NVLink in P2P mode) and reported to its owner only.
+    cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid(),
+                       transport=tp)
+    opt = bl.Optimizer("onebit_lamb", sizes, hp, cl)
+    for t in range(3):
+        g = (rng.standard_normal((1, d)) * sig).astype(np.float32)
+        bad = t == 2 and rank == world - 1
+        if bad:
+            g[0, 5] = np.nan
+        try:
+            opt.step(g, t, 1e-3)
+            raised = ""
+        except Exception as exc:  # noqa: BLE001 - the message is checked below
+            raised = str(exc)
+        if bad:
+            check("non-finite gradient" in raised and f"worker {world - 1}" in raised,
+                  f"{tp} non-finite gradient reported to its owner: {raised!r}")
+        else:
+            check(raised == "", f"{tp} rank {rank} t={t} unexpected error {raised!r}")
     opt.close()
     cl.close()
 
