@@ -222,12 +222,17 @@ def main():
         if rank != 0:
             return
         ref = run_reference(args, layout, d, n)
-        line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": "ms",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        line = {"impl": "reference",
+                "metric": METRIC if args.workload == "bert-large" else f"1-bit LAMB step time, {args.workload}",
+                "value": ref["value"], "unit": "ms",
+                "n_gpus": args.gpus if world == 1 else world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ref["value"], "higher_is_better": False, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"{args.workload} compression-stage step, n={n} workers",
-                           "params": d, "layers": len(sizes)},
+                # the same workload as our arm's line; the reference runs its
+                # n data-parallel workers as simulated workers on the host
+                "config": {"workload": f"{args.workload} 1-bit LAMB compression-stage step",
+                           "params": d, "layers": len(sizes), "world": n,
+                           "mode": "reference CPU, simulated workers", "parallelism": f"dp{n}"},
                 "cpu_baseline": ref,
                 "e2e": {"value": ref["value"], "unit": "ms", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}

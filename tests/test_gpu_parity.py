@@ -286,7 +286,7 @@ def run_pair(bl, sizes, n, steps, warmup, seed, lr=1e-3, wd=0.0, scaled=False, c
     return opt, oopt, cl, ocl
 
 
-@pytest.mark.parametrize("n", [1, 2, 4])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
 def test_optimizer_onebit_lamb_bitexact_vs_oracle_f32(bl, n):
     sizes = [3000, 2, 1024, 1023, 5000, 3, 4096 * 3 + 17]
     opt, oopt, cl, ocl = run_pair(bl, sizes, n, steps=30, warmup=8, seed=5 + n)
