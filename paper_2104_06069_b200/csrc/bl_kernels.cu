@@ -561,12 +561,13 @@ __global__ void __launch_bounds__(kBlock, K1_MINB) k1_worker_compress(const K1Pa
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const long long per_w = static_cast<long long>(p.n) * p.tpc;
-  const long long total = p.slow_list ? static_cast<long long>(p.n_slow) * p.nw : per_w * p.nw;
+  const long long total = p.slow_list ? static_cast<long long>(p.n_slow) * p.nw
+                                      : (p.tile_cnt ? p.tile_cnt : per_w * p.nw);
   const float es = p.es_dev ? __ldg(p.es_dev) : p.es_host;
 
   TileSched sch{p.slow_list ? nullptr : p.ctr, total, nwarps, 0};
   for (long long it = sch.first(gw, lane); it < total; it = sch.next(lane)) {
-    long long tile = it;
+    long long tile = it + p.tile_lo;
     if (p.slow_list) {  // iterate only the listed boundary tiles of every worker
       const long long wl = it / p.n_slow;
       tile = wl * per_w + __ldg(p.slow_list + (it - wl * p.n_slow));

@@ -67,6 +67,7 @@ struct K1Params {
   const int* slow_list;       // general kernel after k1_bulk: the non-fast (j*tpc+t) tiles
   int n_slow;
   unsigned int* ctr;          // dynamic tile counter (self-resetting) or nullptr
+  long long tile_lo, tile_cnt;  // register path: tiles [tile_lo, tile_lo + tile_cnt) (cnt 0: all)
 };
 
 // K3: server reduction of chunk(s) owned locally.

@@ -177,7 +177,48 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
     p.rx_off = my_slot;
   }
   cudaEvent_t a;
-  if (k1_uses_bulk(p, k1_mode)) {  // bulk fast tiles, then the boundary tiles
+  const float* host = stage_host;
+  stage_host = nullptr;
+  if (host && k1_uses_bulk(p, k1_mode)) {  // no piecewise K1 on the bulk path: copy first
+    const float* srcs[1] = {host};
+    copy_inputs(srcs, 1, dim, BL_MEM_HOST);
+    host = nullptr;
+  }
+  if (host) {
+    // Tile-aligned pieces of the H2D copy on a copy stream; the K1 launch of
+    // each piece waits only for its own bytes.  Tiles are in element order
+    // (chunk j's tiles cover [j*c, (j+1)*c)), so piece k is a contiguous range.
+    if (!copy_stream) {
+      cuda_check(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "copy stream");
+      for (auto& e : piece_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    const long long T = static_cast<long long>(n) * tpc;
+    const int M = static_cast<int>(std::min<long long>(kPieces, T));
+    auto elem = [&](long long tile) -> uint64_t {
+      if (tile >= T) return dim;
+      const uint64_t e = static_cast<uint64_t>(tile / tpc) * c + static_cast<uint64_t>(tile % tpc) * kTile;
+      return std::min<uint64_t>(e, dim);
+    };
+    cuda_check(cudaEventRecord(piece_ev[kPieces], stream), "event");  // `in` free to overwrite
+    cuda_check(cudaStreamWaitEvent(copy_stream, piece_ev[kPieces], 0), "wait");
+    begin(KC_K1, &a);
+    int launched = 0;
+    for (int k = 0; k < M; ++k) {
+      const long long t0 = T * k / M, t1 = T * (k + 1) / M;
+      const uint64_t e0 = elem(t0), e1 = elem(t1);
+      if (e1 > e0)
+        cuda_check(cudaMemcpyAsync(in + e0, host + e0, (e1 - e0) * sizeof(float), cudaMemcpyHostToDevice,
+                                   copy_stream),
+                   "cudaMemcpyAsync(piece)");
+      cuda_check(cudaEventRecord(piece_ev[k], copy_stream), "event");
+      cuda_check(cudaStreamWaitEvent(stream, piece_ev[k], 0), "wait");
+      K1Params q = p;
+      q.tile_lo = t0;
+      q.tile_cnt = t1 - t0;
+      launched += launch_k1(q, k1_mode, grid(t1 - t0), stream);
+    }
+    end(KC_K1, a, launched);
+  } else if (k1_uses_bulk(p, k1_mode)) {  // bulk fast tiles, then the boundary tiles
     begin(KC_K1, &a);
     end(KC_K1, a, launch_k1_phase(p, k1_mode, 0, stream));
     begin(KC_K1B, &a);
@@ -765,7 +806,16 @@ void bl_optimizer::step(const float* const* grads, int n_grads, uint64_t t, doub
            "compression-stage step before warmup finalized: frozen variance, c_avg and momentum "
            "snapshot are missing");
     }
-    cl->copy_inputs(grads, n_grads, d, memory);
+    // Host gradients in the one-bit compression stage: the H2D copy is cut
+    // into tile-aligned pieces and K1 starts on each piece as it lands
+    // (bl_cluster::compressed).  BL_OVERLAP_H2D=0 copies first.
+    const char* ov = std::getenv("BL_OVERLAP_H2D");
+    if (memory == BL_MEM_HOST && cl->nw == 1 && cl->cfg.compressor == BL_COMPRESSOR_ONEBIT &&
+        !(ov && ov[0] == '0')) {
+      cl->stage_host = grads[0];
+    } else {
+      cl->copy_inputs(grads, n_grads, d, memory);
+    }
     compressed_step(lr);
     compressed = true;
   }
@@ -980,6 +1030,10 @@ void bl_cluster_destroy(bl_cluster* c) {
     cudaEventDestroy(e.b);
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->copy_stream) {
+    for (auto e : c->piece_ev) cudaEventDestroy(e);
+    cudaStreamDestroy(c->copy_stream);
+  }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }

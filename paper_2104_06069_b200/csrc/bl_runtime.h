@@ -101,6 +101,13 @@ struct bl_cluster {
   int* k1_slow = nullptr;       // API-mode K1 tiles that are not full/inside the data
   int k1_n_slow = 0;
 
+  // Host gradient staged for the next compressed collective: copied in
+  // pieces that K1 consumes as they land (optimizer step, BL_MEM_HOST).
+  const float* stage_host = nullptr;
+  static constexpr int kPieces = 16;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t piece_ev[kPieces + 1] = {};
+
   uint64_t checks = 0;          // compensation checks run (comm_sim.hpp:110)
   bool verify_es_one = true;    // the optimizer's device error scale is 1 (no scaled EF)
   void verify_last();           // verify_compensation over the local endpoints
