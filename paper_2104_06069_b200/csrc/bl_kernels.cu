@@ -284,8 +284,9 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// After one explicit system fence, further flags need no fence of their own.
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Thread 0 of the block waits until flags[0..n) >= epoch (bounded: a peer that
@@ -872,23 +873,52 @@ __device__ __forceinline__ double stripe_sum(const double* a, long long t0, long
   return s;
 }
 
-__global__ void __launch_bounds__(1024) k_finalize_scales(const FinalizeParams p) {
-  __shared__ double sh[32];
-  const int e = blockIdx.x;
-  const double* part = p.partials + static_cast<size_t>(e) * p.tpc;
-  double s = stripe_sum(part, threadIdx.x, p.tpc);
-  s = block1024_sum(s, sh);
-  if (threadIdx.x == 0) {
+// Endpoint e's scale from its combined partial sum s (compression.cpp:54-58):
+// local slot, finite check and, for the fused exchange, the peers' slots and
+// epoch flags.  One thread.
+__device__ void finalize_commit(const FinalizeParams& p, int e, double s) {
+  {
     const float S = static_cast<float>(s / static_cast<double>(p.c));
     p.slots[static_cast<size_t>(e) * p.slot_stride + p.W] = __float_as_uint(S);
     if (!isfinite(S)) flag(p.err, kErrScale, static_cast<unsigned long long>(p.err_base + e));
     if (p.peer_slots) {
       const int q0 = p.to_all ? 0 : e, q1 = p.to_all ? p.n : e + 1;
       for (int q = q0; q < q1; ++q) p.peer_slots[q][p.peer_off + p.W] = __float_as_uint(S);
-      __threadfence_system();
-      for (int q = q0; q < q1; ++q) st_release_sys(p.peer_flags[q] + p.flag_index, p.epoch);
+      __threadfence_system();  // the scale words before any flag
+      for (int q = q0; q < q1; ++q) st_relaxed_sys(p.peer_flags[q] + p.flag_index, p.epoch);
     }
   }
+}
+
+__global__ void __launch_bounds__(1024) k_finalize_scales(const FinalizeParams p) {
+  __shared__ double sh[32];
+  const int e = blockIdx.x;
+  const double* part = p.partials + static_cast<size_t>(e) * p.tpc;
+  double s = stripe_sum(part, threadIdx.x, p.tpc);
+  s = block1024_sum(s, sh);
+  if (threadIdx.x == 0) finalize_commit(p, e, s);
+}
+
+// The same canonical combine with a 256-thread block (fused small
+// collective): thread i forms stripes i, i+256, i+512, i+768; warp w
+// butterflies stripe groups w, w+8, w+16, w+24 (32 stripes each); warp 0
+// butterflies the 32 group sums — k_finalize_scales' order exactly.
+__device__ void finalize_block256(const FinalizeParams& p, int e, double* red /* [1024 + 32] */) {
+  const double* part = p.partials + static_cast<size_t>(e) * p.tpc;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int k = 0; k < 4; ++k) red[tid + 256 * k] = stripe_sum(part, tid + 256 * k, p.tpc);
+  __syncthreads();
+  for (int k = 0; k < 4; ++k) {
+    const int g = w + 8 * k;
+    const double v = warp_bfly_sum(red[32 * g + lane]);
+    if (lane == 0) red[1024 + g] = v;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const double v = warp_bfly_sum(red[1024 + lane]);
+    if (lane == 0) finalize_commit(p, e, v);
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -1875,7 +1905,7 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
   if (threadIdx.x == 0 && atomicAdd(p.done, 1u) == gridDim.x - 1) {
     *p.done = 0u;
     __threadfence_system();
-    for (int q = 0; q < p.n; ++q) st_release_sys(p.peer_flags[q] + p.out_flag + p.rank, p.epoch);
+    for (int q = 0; q < p.n; ++q) st_relaxed_sys(p.peer_flags[q] + p.out_flag + p.rank, p.epoch);
   }
 }
 
@@ -1883,7 +1913,7 @@ __global__ void k_signal_peers(unsigned long long* const* peer_flags, int index,
                                unsigned long long epoch) {
   if (threadIdx.x == 0) {
     __threadfence_system();
-    for (int q = 0; q < n; ++q) st_release_sys(peer_flags[q] + index, epoch);
+    for (int q = 0; q < n; ++q) st_relaxed_sys(peer_flags[q] + index, epoch);
   }
 }
 
@@ -1891,12 +1921,10 @@ __global__ void k_signal_peers(unsigned long long* const* peer_flags, int index,
 // chunk-relative, one warp per 32 packet words (1024 elements): every lane
 // reads the same word (broadcast) and writes one element of each 32-element
 // group (coalesced), truncated at c and d.
-__global__ void k_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
-                             uint64_t d, float* out) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void decompress_warps(const uint32_t* res, int n, uint64_t c, uint64_t slot,
+                                                 uint64_t W, uint64_t d, float* out, uint64_t gw,
+                                                 uint64_t nwarps, int lane) {
   const uint64_t groups = (W + 31) / 32;  // 32-word groups per chunk
-  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t g = gw; g < groups * n; g += nwarps) {
     const uint64_t j = g / groups, w0 = (g - j * groups) * 32;
     const uint32_t* sl = res + j * slot;
@@ -1911,6 +1939,305 @@ __global__ void k_decompress(const uint32_t* res, int n, uint64_t c, uint64_t sl
       if (e < c && kc + e < d) out[kc + e] = (word >> lane) & 1u ? pos : neg;
     }
   }
+}
+
+__global__ void k_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
+                             uint64_t d, float* out) {
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  decompress_warps(res, n, c, slot, W, d, out, gw, nwarps, threadIdx.x & 31);
+}
+
+// ---------------------------------------------------------------------------
+// Fused small compressed collective (P2P transport): K1 -> worker scales ->
+// exchange -> K3 -> server scale -> exchange [-> decompress] in one
+// cooperative kernel.  Below ~64 MB the separate kernels are latency-bound
+// (7 launches, each a ramp, a tail and a system fence); here the phases are
+// separated by grid barriers and the peers' epoch flags only.  Every
+// per-element operation and reduction order is the unfused path's.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      long long spins = 0;
+      while (*gen == g && ++spins < (1ll << 30)) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// One K1 tile per CTA: warp w computes rows 4w..4w+3 in a single load batch;
+// |corr| goes to shared memory and warp 0 sums it in the canonical per-lane
+// order (rows 0..31, elements 4l..4l+3), so the tile partial is the warp
+// path's bit for bit.  Tiles off the fast path are done by warp 0 alone.
+template <int MODE, bool ALIGNED>
+__device__ __forceinline__ void k1_cta_tile(const K1Params& p, long long tile, uint32_t* sw,
+                                            float* s_abs, float* s_cm, float es) {
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const long long per_w = static_cast<long long>(p.n) * p.tpc;
+  const int w = static_cast<int>(tile / per_w);
+  const long long rem = tile - w * per_w;
+  const int j = static_cast<int>(rem / p.tpc);
+  const int t = static_cast<int>(rem - static_cast<long long>(j) * p.tpc);
+  const uint64_t i0 = static_cast<uint64_t>(t) * kTile;
+  const uint64_t kc = static_cast<uint64_t>(j) * p.c;
+  bool fast = MODE != 1 && i0 + kTile <= p.c && kc + i0 + kTile <= p.d;
+  float A = 0.f, B = 0.f, IC = 0.f;
+  if (fast && MODE == 2) {
+    int l0;
+    if (p.tile_layer) {
+      l0 = __ldg(p.tile_layer + static_cast<size_t>(j) * p.tpc + t);
+      fast = l0 >= 0;
+    } else {
+      l0 = find_layer(p.off, p.L, kc + i0);
+      fast = l0 < p.L && kc + i0 + (kTile - 1) < __ldg(p.off + l0 + 1);
+    }
+    if (fast) {
+      A = __ldg(p.A + l0);
+      B = __ldg(p.B + l0);
+      IC = __ldg(p.invc + l0);
+    }
+  }
+  if (!fast) {
+    if (wq == 0) k1_tile<MODE, ALIGNED>(p, tile, lane, sw, es);
+    __syncthreads();
+    return;
+  }
+  const int s = ALIGNED ? 0 : static_cast<int>(kc & 3u);
+  const size_t ep = static_cast<size_t>(w) * p.n + j;
+  const float* gin = p.in + static_cast<size_t>(w) * p.in_stride + kc + i0;
+  float* we = p.werr + ep * p.c_pad + i0;
+  const uint32_t* pkp = p.pk_prev + ep * p.slot;
+  const float Sp = slot_scale(pkp, p.W);
+  pkp += i0 >> 5;
+  float pos_m = 0.f, neg_m = 0.f;
+  const uint32_t* rp = nullptr;
+  if (MODE == 2) {
+    const uint32_t* rs = p.res_prev + static_cast<size_t>(j) * p.slot;
+    const float S2 = slot_scale(rs, p.W);
+    pos_m = S2;
+    neg_m = S2 == 0.0f ? 0.0f : -S2;
+    rp = rs + (i0 >> 5);
+  }
+  constexpr int R = 4;
+  const int r0 = R * wq;
+  const uint32_t sh = 4 * (lane & 7);
+  const int wsub = lane >> 3;
+  float4 g[R], raw[R];
+  uint32_t wn[R], rn[R];
+  load_rows<R, true>(g, gin + r0 * kRowElems, lane, s);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    raw[k] = ldg_rw(we + (r0 + k) * kRowElems + 4 * lane);
+    wn[k] = __ldg(pkp + 4 * (r0 + k) + wsub) >> sh;
+    rn[k] = MODE == 2 ? __ldg(rp + 4 * (r0 + k) + wsub) >> sh : 0u;
+  }
+  float cm = 0.0f;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (MODE == 2 && !(isfinite(g[k].x) && isfinite(g[k].y) && isfinite(g[k].z) && isfinite(g[k].w))) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!isfinite(comp(g[k], q)))
+          flag(p.err, kErrGrad, (static_cast<unsigned long long>(p.worker_base + w) << 40) |
+                                    (kc + i0 + (r0 + k) * kRowElems + 4 * lane + q));
+    }
+    uint32_t nib = 0;
+    float4 rawn, ab;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float v;
+      if (MODE == 0) {
+        v = comp(g[k], q);
+      } else {
+        const float mq = __fmul_rn((rn[k] >> q) & 1u ? pos_m : neg_m, IC);  // fusion.cpp:143
+        v = __fadd_rn(__fmul_rn(A, mq), __fmul_rn(B, comp(g[k], q)));    // kernels.cpp:253
+      }
+      const float rec = (wn[k] >> q) & 1u ? Sp : -Sp;
+      const float delta = __fsub_rn(comp(raw[k], q), rec);               // compression.cpp:194
+      const float corr = __fadd_rn(v, __fmul_rn(es, delta));             // :181
+      set_comp(rawn, q, __fadd_rn(v, delta));
+      nib |= static_cast<uint32_t>(corr >= 0.0f) << q;                   // :50
+      set_comp(ab, q, fabsf(corr));
+      cm = cm < fabsf(corr) ? fabsf(corr) : cm;
+    }
+    st4(we + (r0 + k) * kRowElems + 4 * lane, rawn);
+    *reinterpret_cast<float4*>(s_abs + (r0 + k) * kRowElems + 4 * lane) = ab;
+    stage_row_bits(sw, r0 + k, lane, nib);
+  }
+  cm = warp_max(cm);
+  if (lane == 0) s_cm[wq] = cm;
+  __syncthreads();
+  if (wq == 0) {
+    double acc = 0.0;  // :54, the warp path's per-lane order
+    for (int r = 0; r < kRowsPerTile; ++r) {
+      const float4 ab = *reinterpret_cast<const float4*>(s_abs + r * kRowElems + 4 * lane);
+      acc += static_cast<double>(ab.x);
+      acc += static_cast<double>(ab.y);
+      acc += static_cast<double>(ab.z);
+      acc += static_cast<double>(ab.w);
+    }
+    acc = warp_bfly_sum(acc);
+    if (lane == 0) p.partials[ep * p.tpc + t] = acc;
+    if (p.cmax) {
+      const float m = warp_max(lane < kWarpsPerBlock ? s_cm[lane] : 0.0f);
+      if (lane == 0) p.cmax[ep * p.tpc + t] = m;
+    }
+    const uint4 wv = tile_words(sw, lane);
+    reinterpret_cast<uint4*>(p.pk_cur + ep * p.slot + (i0 >> 5))[lane] = wv;
+    if (p.peer_rx) reinterpret_cast<uint4*>(p.peer_rx[j] + p.rx_off + (i0 >> 5))[lane] = wv;
+  }
+  __syncthreads();
+}
+
+// One K3 tile per CTA (rows split over the warps as in k1_cta_tile), general
+// arithmetic: any n, partial tiles (elements past c are dead and add 0).
+__device__ __forceinline__ void k3_cta_tile(const K3Params& p, long long tile, uint32_t* sw,
+                                            float* s_abs, float* s_cm, const float* scale,
+                                            uint32_t* const* peers, float es, double inv_n) {
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int n = p.n;
+  const int t = static_cast<int>(tile);  // ns == 1: server `server_base`
+  const int j = p.server_base;
+  const uint64_t i0 = static_cast<uint64_t>(t) * kTile;
+  float* se = p.serr + i0;
+  const uint32_t* rs = p.res_prev + static_cast<size_t>(j) * p.slot;
+  const float S2p = slot_scale(rs, p.W);
+  rs += i0 >> 5;
+  const uint32_t* inw = p.in + (i0 >> 5);
+  constexpr int R = 4;
+  const int r0 = R * wq;
+  constexpr int kMaxN = 8;  // workers whose nibbles are loaded up front
+  float4 raw[R];
+  uint32_t sn[R], nb[R][kMaxN];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    raw[k] = ld4(se + (r0 + k) * kRowElems + 4 * lane);
+    sn[k] = row_nibble(rs, r0 + k, lane);
+#pragma unroll
+    for (int i = 0; i < kMaxN; ++i)
+      nb[k][i] = i < n ? ld_cg(inw + i * p.in_i + 4 * (r0 + k) + (lane >> 3)) : 0u;
+  }
+  float cm = 0.0f;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int r = r0 + k;
+    const uint64_t ir = i0 + static_cast<uint64_t>(r) * kRowElems;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    auto add = [&](int i, uint32_t word) {  // compression.cpp:83-89, ascending workers
+      const float S = scale[i];
+      const uint32_t b = (word >> (4 * (lane & 7))) & 0xFu;
+      if (S != 0.0f) {
+        const double Sd = S;
+        a0 += (b & 1u) ? Sd : -Sd;
+        a1 += (b & 2u) ? Sd : -Sd;
+        a2 += (b & 4u) ? Sd : -Sd;
+        a3 += (b & 8u) ? Sd : -Sd;
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < kMaxN; ++i)
+      if (i < n) add(i, nb[k][i]);
+    for (int i = kMaxN; i < n; ++i) add(i, ld_cg(inw + i * p.in_i + 4 * r + (lane >> 3)));
+    const float4 avg = make_float4(static_cast<float>(a0 * inv_n), static_cast<float>(a1 * inv_n),
+                                   static_cast<float>(a2 * inv_n), static_cast<float>(a3 * inv_n));
+    uint32_t nib = 0;
+    float4 rawn, ab;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = ir + 4 * lane + q;
+      const float v = comp(avg, q);
+      const float rec = (sn[k] >> q) & 1u ? S2p : -S2p;
+      const float delta = __fsub_rn(comp(raw[k], q), rec);
+      const float corr = __fadd_rn(v, __fmul_rn(es, delta));
+      const bool live = i < p.c;
+      set_comp(rawn, q, live ? __fadd_rn(v, delta) : 0.0f);
+      nib |= static_cast<uint32_t>(live && corr >= 0.0f) << q;
+      set_comp(ab, q, live ? fabsf(corr) : 0.0f);
+      if (live) cm = cm < fabsf(corr) ? fabsf(corr) : cm;
+    }
+    if (ir < p.c) st4(se + r * kRowElems + 4 * lane, rawn);
+    *reinterpret_cast<float4*>(s_abs + r * kRowElems + 4 * lane) = ab;
+    stage_row_bits(sw, r, lane, nib);
+  }
+  cm = warp_max(cm);
+  if (lane == 0) s_cm[wq] = cm;
+  __syncthreads();
+  if (wq == 0) {
+    double acc = 0.0;
+    for (int r = 0; r < kRowsPerTile; ++r) {
+      const float4 ab = *reinterpret_cast<const float4*>(s_abs + r * kRowElems + 4 * lane);
+      acc += static_cast<double>(ab.x);
+      acc += static_cast<double>(ab.y);
+      acc += static_cast<double>(ab.z);
+      acc += static_cast<double>(ab.w);
+    }
+    acc = warp_bfly_sum(acc);
+    if (lane == 0) p.partials[t] = acc;
+    if (p.cmax) {
+      const float m = warp_max(lane < kWarpsPerBlock ? s_cm[lane] : 0.0f);
+      if (lane == 0) p.cmax[t] = m;
+    }
+    flush_server_words(p, peers, sw, p.res_cur + static_cast<size_t>(j) * p.slot + (i0 >> 5), i0, lane);
+  }
+  __syncthreads();
+}
+
+template <int MODE, bool ALIGNED>
+__global__ void __launch_bounds__(kBlock) k_small_collective(__grid_constant__ const SmallParams p) {
+  __shared__ __align__(16) uint32_t s_words[128];  // the CTA's tile packet words
+  __shared__ float s_scale[64];
+  __shared__ uint32_t* s_peer[64];
+  __shared__ double s_red[1024 + 32];
+  __shared__ __align__(16) float s_abs[kTile];
+  __shared__ float s_cm[kWarpsPerBlock];
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const int n = p.k1.n;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) s_peer[q] = p.k3.peer_res[q];
+  // 1. worker compression of every chunk of the local stream; packet words
+  //    go to the local slot and into rank j's receive slot
+  {
+    const float es = p.k1.es_dev ? __ldg(p.k1.es_dev) : p.k1.es_host;
+    const long long total = static_cast<long long>(n) * p.k1.tpc;
+    for (long long tile = blockIdx.x; tile < total; tile += gridDim.x)
+      k1_cta_tile<MODE, ALIGNED>(p.k1, tile, s_words, s_abs, s_cm, es);
+    warp_fence_system(lane);
+  }
+  grid_barrier(p.bar, gridDim.x);
+  // 2. worker scales: block e finalizes endpoint (this worker, chunk e) and
+  //    raises rank e's flag
+  for (int e = blockIdx.x; e < n; e += gridDim.x) finalize_block256(p.f1, e, s_red);
+  // 3. every worker's packet for this rank's chunk has arrived
+  wait_peers(p.flags, n, p.epoch, p.err);
+  // 4. server reduce of chunk `rank`; server words into every rank's result slot
+  {
+    const float es = p.k3.es_dev ? __ldg(p.k3.es_dev) : p.k3.es_host;
+    const double inv_n = 1.0 / static_cast<double>(n);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s_scale[i] = slot_scale_cg(p.k3.in + i * p.k3.in_i, p.k3.W);
+    __syncthreads();
+    for (long long tile = blockIdx.x; tile < p.k3.tpc; tile += gridDim.x)
+      k3_cta_tile(p.k3, tile, s_words, s_abs, s_cm, s_scale, s_peer, es, inv_n);
+    warp_fence_system(lane);
+  }
+  grid_barrier(p.bar, gridDim.x);
+  // 5. server scale to every rank, flags
+  if (blockIdx.x == 0) finalize_block256(p.f2, 0, s_red);
+  // 6. every rank's server packet has arrived; 7. optional decompress
+  wait_peers(p.flags + n, n, p.epoch, p.err);
+  if (p.out)
+    decompress_warps(p.res, n, p.k3.c, p.k3.slot, p.k3.W, p.d, p.out, static_cast<uint64_t>(gw),
+                     static_cast<uint64_t>(nwarps), lane);
 }
 
 __global__ void k_materialize_error(const float* raw, uint64_t c_pad, const uint32_t* pk,
@@ -2235,6 +2562,34 @@ int launch_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const fl
                         unsigned long long* err, int worker_base, cudaStream_t s) {
   k_build_stream<<<grid_for_elems(d), 256, 0, s>>>(in, stride, nw, d, m, off, L, A, B, err, worker_base);
   return 1;
+}
+
+template <int MODE, bool ALIGNED>
+static int launch_small_t(const SmallParams& p, long long tiles, cudaStream_t s) {
+  auto kern = k_small_collective<MODE, ALIGNED>;
+  static thread_local int cap = 0;  // co-resident blocks (cooperative launch)
+  if (cap == 0) {
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, 0);
+    cap = sms * (occ > 0 ? occ : 1);
+  }
+  long long want = tiles;            // one CTA per tile
+  if (want < p.k1.n) want = p.k1.n;  // one block per worker endpoint
+  const int grid = static_cast<int>(std::min<long long>(want, cap));
+  void* args[] = {const_cast<SmallParams*>(&p)};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), grid, kBlock,
+                                                    args, 0, s);
+  return e == cudaSuccess ? 1 : -static_cast<int>(e);
+}
+
+int launch_small_collective(const SmallParams& p, int k1_mode, cudaStream_t s) {
+  const long long tiles = static_cast<long long>(p.k1.n) * p.k1.tpc;
+  const bool al = (p.k1.c & 3u) == 0;
+  if (k1_mode == 0) return al ? launch_small_t<0, true>(p, tiles, s) : launch_small_t<0, false>(p, tiles, s);
+  if (k1_mode == 1) return launch_small_t<1, false>(p, tiles, s);
+  return al ? launch_small_t<2, true>(p, tiles, s) : launch_small_t<2, false>(p, tiles, s);
 }
 
 int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s) {

@@ -178,6 +178,21 @@ struct K6Params {
   const float* dense;  // identity compressor: dense result
 };
 
+// Fused small compressed collective (P2P transport, one cooperative kernel).
+struct SmallParams {
+  K1Params k1;
+  FinalizeParams f1;   // worker endpoints (this rank's n chunk packets)
+  K3Params k3;
+  FinalizeParams f2;   // server endpoint (chunk `rank`)
+  const unsigned long long* flags;  // local [2n]: worker packets in, server packets in
+  unsigned long long epoch;
+  unsigned long long* err;
+  unsigned int* bar;   // grid barrier [2] (count, generation)
+  float* out;          // decompressed result [d] or nullptr
+  const uint32_t* res; // result packets [n][slot] (this call's)
+  uint64_t d;
+};
+
 // Deterministic lossless all-reduce over NVLink peer memory (P2P transport).
 struct LosslessP2PParams {
   const float* const* peer_in;            // [n] every rank's gradient buffer
@@ -273,6 +288,8 @@ int launch_verify(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t
                   uint64_t c, uint64_t len, double tol, unsigned long long* err, cudaStream_t s);
 // Block the stream until flags[0..n) >= epoch (peer signals, bounded wait).
 int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s);
+// Returns 1, or -cudaError when the cooperative launch is refused.
+int launch_small_collective(const SmallParams& p, int k1_mode, cudaStream_t s);
 // Raise flag `index` (+ own rank) at every peer to `epoch` after this stream's
 // prior work (system-scope release).
 int launch_signal_peers(unsigned long long* const* peer_flags, int index, int n,

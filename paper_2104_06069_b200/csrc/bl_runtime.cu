@@ -25,7 +25,7 @@ const char* const kClassNames[KC_COUNT] = {
     "layer_epilogue",     "k6_update_b",     "w1_warmup_a",      "warmup_epilogue",
     "w2_warmup_b",        "average",         "decompress",       "materialize",
     "endpoint_stats",     "nccl_alltoall",   "nccl_allgather",   "h2d_copy",
-    "d2h_copy",           "k1_boundary_tiles"};
+    "d2h_copy",           "k1_boundary_tiles", "small_collective"};
 
 void fail(bl_status st, const std::string& msg) { throw Error{st, msg}; }
 
@@ -143,7 +143,8 @@ void bl_cluster::copy_inputs(const float* const* inputs, int n_inputs, uint64_t 
   end(KC_H2D, a, 0);
 }
 
-void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, const float* es_dev) {
+bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, const float* es_dev,
+                            float* dec_out) {
   K1Params p = ovr ? *ovr : K1Params{};
   if (!ovr) {
     p.slow_list = k1_slow;
@@ -179,6 +180,76 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
   cudaEvent_t a;
   const float* host = stage_host;
   stage_host = nullptr;
+  // Small collectives over NVLink: one cooperative kernel for the whole
+  // exchange (and the decompress, when asked).  BL_SMALL_MAX_TILES sets the
+  // size limit (K1 tiles per rank; 0 disables).
+  const char* sm_env = std::getenv("BL_SMALL_MAX_TILES");
+  const long long small_max = sm_env ? std::atoll(sm_env) : 2048;
+  if (p2p && nw == 1 && static_cast<long long>(n) * tpc <= small_max) {
+    if (host) {  // small: copy the staged host gradient first
+      const float* srcs[1] = {host};
+      copy_inputs(srcs, 1, dim, BL_MEM_HOST);
+    }
+    SmallParams sp{};
+    sp.k1 = p;
+    sp.k1.slow_list = nullptr;  // every tile through k1_tile
+    sp.k1.n_slow = 0;
+    sp.k1.skip_fast = 0;
+    sp.f1 = FinalizeParams{wpart, tpc, c, wpk[cur()], slot, W, err, p.worker_base * n};
+    sp.f1.peer_slots = d_peer_rx;
+    sp.f1.peer_off = my_slot;
+    sp.f1.peer_flags = d_peer_flags;
+    sp.f1.flag_index = rank;
+    sp.f1.to_all = 0;
+    sp.f1.n = n;
+    sp.f1.epoch = epoch;
+    K3Params& k3 = sp.k3;
+    k3.n = n;
+    k3.ns = 1;
+    k3.tpc = tpc;
+    k3.server_base = rank;
+    k3.c = c;
+    k3.c_pad = c_pad;
+    k3.slot = slot;
+    k3.W = W;
+    k3.in = rx + static_cast<size_t>(cur()) * n * slot;
+    k3.in_s = 0;
+    k3.in_i = slot;
+    k3.serr = serr;
+    k3.res_prev = res[prev()];
+    k3.res_cur = res[cur()];
+    k3.es_dev = es_dev;
+    k3.es_host = es_host;
+    k3.partials = spart;
+    k3.cmax = cfg.endpoint_stats ? scmax : nullptr;
+    k3.err = err;
+    k3.peer_res = d_peer_res;
+    k3.res_off = my_slot;
+    k3.rank = rank;
+    sp.f2 = FinalizeParams{spart, tpc, c, res[cur()] + static_cast<size_t>(rank) * slot, slot, W, err,
+                           1 << 20};
+    sp.f2.peer_slots = d_peer_res;
+    sp.f2.peer_off = my_slot;
+    sp.f2.peer_flags = d_peer_flags;
+    sp.f2.flag_index = n + rank;
+    sp.f2.to_all = 1;
+    sp.f2.n = n;
+    sp.f2.epoch = epoch;
+    sp.flags = flags;
+    sp.epoch = epoch;
+    sp.err = err;
+    sp.bar = small_bar;
+    sp.out = dec_out;
+    sp.res = res[cur()];
+    sp.d = dim;
+    begin(KC_SMALL, &a);
+    const int r = launch_small_collective(sp, k1_mode, stream);
+    if (r < 0) fail(BL_ERR_CUDA, std::string("fused small collective launch: ") +
+                                    cudaGetErrorString(static_cast<cudaError_t>(-r)));
+    end(KC_SMALL, a, r);
+    finish_compressed(es_host, es_dev);
+    return dec_out != nullptr;
+  }
   if (host && k1_uses_bulk(p, k1_mode)) {  // no piecewise K1 on the bulk path: copy first
     const float* srcs[1] = {host};
     copy_inputs(srcs, 1, dim, BL_MEM_HOST);
@@ -325,6 +396,11 @@ void bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
                "ncclAllGather");
     end(KC_AG, a, 0);
   }
+  finish_compressed(es_host, es_dev);
+  return false;
+}
+
+void bl_cluster::finish_compressed(float es_host, const float* es_dev) {
   calls += 1;
   last_identity = false;
   ledger_compressed();
@@ -340,6 +416,7 @@ void bl_cluster::setup_p2p(bool required) {
   rx = dalloc<uint32_t>(2 * nn * slot);
   flags = reinterpret_cast<unsigned long long*>(dalloc<double>(4 * nn));
   lossless_done = reinterpret_cast<unsigned int*>(dalloc<float>(1));
+  small_bar = reinterpret_cast<unsigned int*>(dalloc<float>(2));
   // Buffers every peer maps: packet receive slots, result packets, flags,
   // gradient (lossless reads), output (lossless allgather), error words.
   constexpr int kB = 6;
@@ -1022,7 +1099,7 @@ void bl_cluster_destroy(bl_cluster* c) {
                   c->scmax,     c->out,        c->lrecv,           c->err,       c->stat_part,
                   c->stat_max,  c->stat_out,   c->rx,              c->flags,     c->d_peer_rx,
                   c->d_peer_res, c->d_peer_flags, c->d_peer_in, c->d_peer_out, c->d_peer_err,
-                  c->lossless_done, c->k1_slow, c->tile_ctr};
+                  c->lossless_done, c->small_bar, c->k1_slow, c->tile_ctr};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& e : c->pending) {
@@ -1065,12 +1142,13 @@ bl_status bl_cluster_compressed_allreduce(bl_cluster* c, const float* const* inp
       if (c->cfg.verify_compensation && error_scale == 1.0)  // v + 0 == v + 0 exactly
         c->checks += static_cast<uint64_t>(c->nw) * c->n + static_cast<uint64_t>(c->ns);
     } else {
-      c->compressed(nullptr, 0, static_cast<float>(error_scale), nullptr);
-      const int latest = static_cast<int>((c->calls + 1u) & 1u);
-      cudaEvent_t a;
-      c->begin(KC_DEC, &a);
-      c->end(KC_DEC, a, launch_decompress(c->res[latest], c->n, c->c, c->slot, c->W, c->dim, c->out,
-                                          c->stream));
+      if (!c->compressed(nullptr, 0, static_cast<float>(error_scale), nullptr, c->out)) {
+        const int latest = static_cast<int>((c->calls + 1u) & 1u);
+        cudaEvent_t a;
+        c->begin(KC_DEC, &a);
+        c->end(KC_DEC, a, launch_decompress(c->res[latest], c->n, c->c, c->slot, c->W, c->dim, c->out,
+                                            c->stream));
+      }
     }
     c->pending_is_step = false;
     if (outp) {

@@ -43,7 +43,7 @@ class DeviceGuard {
 // Kernel classes for launch counting and optional CUDA-event timing.
 enum KClass : int {
   KC_K1 = 0, KC_FIN, KC_K3, KC_K5, KC_EPI, KC_K6, KC_W1, KC_WEPI, KC_W2, KC_AVG,
-  KC_DEC, KC_MAT, KC_STATS, KC_A2A, KC_AG, KC_H2D, KC_D2H, KC_K1B, KC_COUNT
+  KC_DEC, KC_MAT, KC_STATS, KC_A2A, KC_AG, KC_H2D, KC_D2H, KC_K1B, KC_SMALL, KC_COUNT
 };
 extern const char* const kClassNames[KC_COUNT];
 
@@ -93,6 +93,7 @@ struct bl_cluster {
   float** d_peer_out = nullptr;       // [n] peers' output buffers
   unsigned long long** d_peer_err = nullptr;  // [n] peers' error words
   unsigned int* lossless_done = nullptr;
+  unsigned int* small_bar = nullptr;  // grid barrier of the fused small collective
   unsigned long long lcalls = 0;      // lossless collectives run (flag epoch)
   std::vector<void*> ipc_opened;
   void setup_p2p(bool required);
@@ -141,8 +142,11 @@ struct bl_cluster {
   void copy_inputs(const float* const* inputs, int n_inputs, uint64_t len, int memory);
   // One compressed collective over the inputs already in `in` (mode 0) or a
   // stream built by the optimizer (K1 params supplied by the caller).
-  void compressed(const bl::K1Params* k1_override, int k1_mode, float es_host,
-                  const float* es_dev);
+  // Returns true when the result was also decompressed into dec_out (the
+  // fused small-collective path).
+  bool compressed(const bl::K1Params* k1_override, int k1_mode, float es_host,
+                  const float* es_dev, float* dec_out = nullptr);
+  void finish_compressed(float es_host, const float* es_dev);
   void lossless(bool check_finite);  // in -> out (averaged), ledger
   void refresh_stats();
   void check_errors(const std::vector<uint64_t>* layer_off);
