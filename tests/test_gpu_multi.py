@@ -18,12 +18,19 @@ def n_gpus() -> int:
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+# "fused": collectives up to 2048 tiles per rank run as the cooperative
+# small-collective kernel (every size the check uses); "split": the same
+# checks through the separate K1 / finalize / K3 kernels (BL_SMALL_MAX_TILES=0).
+@pytest.mark.parametrize("path", ["fused", "split"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_nccl_mode_matches_sim_mode(world):
+def test_nccl_mode_matches_sim_mode(world, path):
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world),
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world + (10 if path == "split" else 0)),
            os.path.join(ROOT, "tests", "multigpu_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ)
+    if path == "split":
+        env["BL_SMALL_MAX_TILES"] = "0"
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0 and "MULTIGPU PASS" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
