@@ -89,6 +89,37 @@ def main() -> int:
         if sim:
             sim.close()
 
+    # ---- 1b. endpoint statistics and verify_compensation -------------------
+    # comm_sim.cpp:108-118,175-180: rank r refreshes its own endpoints
+    # (worker r, server r); they must equal the simulated cluster's.
+    for tp in transports:
+        d = 50_001
+        cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid(),
+                           transport=tp, endpoint_stats=True, verify_compensation=True,
+                           compensation_tolerance=2.0 ** -20)
+        sim = bl.SimCluster(world, d, device=local, endpoint_stats=True) if rank == 0 else None
+        rng = np.random.default_rng(11)
+        for step in range(3):
+            x = rng.standard_normal((world, d)).astype(np.float32)
+            cl.compressed_allreduce(x[rank])
+            ws, ss = cl.worker_stats()[rank], cl.server_stats()[rank]
+            mine = np.array([ws.delta_l2, ws.delta_linf, ws.corrected_linf, ws.max_delta_linf,
+                             ws.max_corrected_linf, ss.delta_l2, ss.delta_linf, ss.corrected_linf,
+                             ss.max_delta_linf, ss.max_corrected_linf])
+            allst = gather_bytes(mine.tobytes())
+            if rank == 0:
+                sim.compressed_allreduce(x)
+                for r in range(world):
+                    w2, s2 = sim.worker_stats()[r], sim.server_stats()[r]
+                    ref = np.array([w2.delta_l2, w2.delta_linf, w2.corrected_linf, w2.max_delta_linf,
+                                    w2.max_corrected_linf, s2.delta_l2, s2.delta_linf, s2.corrected_linf,
+                                    s2.max_delta_linf, s2.max_corrected_linf])
+                    check(allst[r] == ref.tobytes(), f"{tp} endpoint stats rank {r} step {step}")
+        check(cl.compensation_checks() == 3 * (world + 1), f"{tp} compensation checks {cl.compensation_checks()}")
+        cl.close()
+        if sim:
+            sim.close()
+
     # ---- 2. optimizer: warmup + freeze + compression stage -----------------
     for tp in transports:
         optimizer_check(rank, world, local, new_uid, check, tp)
