@@ -1872,6 +1872,9 @@ __device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint
   }
 }
 
+#ifndef LOSSLESS_U
+#define LOSSLESS_U 2  // 4-float groups per thread per iteration (n = 2, 4)
+#endif
 template <int NT>
 __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p) {
   wait_peers(p.in_flags, p.n, p.epoch, p.err);  // every rank's gradient is in place
@@ -1882,7 +1885,7 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
   const uint64_t a1 = dn > a0 ? dn : a0;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  constexpr int U = NT == 8 ? 1 : 2;
+  constexpr int U = NT == 8 ? 1 : LOSSLESS_U;
   for (uint64_t k = a0 + 4 * tid; k < a1; k += 4 * nth * U)
     lossless_groups<NT, U>(p, k, 4 * nth, a1, inv_n);
   if (blockIdx.x == 0) {  // unaligned head [lo, a0) and tail [a1, hi), one element per thread
