@@ -260,6 +260,7 @@ __device__ __forceinline__ void flag(unsigned long long* err, int slot, unsigned
 struct TileSched {
   unsigned int* ctr;
   long long total, nwarps, cur;
+  const int* order = nullptr;  // dynamic mode: hand out order[v] instead of v
   __device__ __forceinline__ long long first(long long gw, int lane) {
     cur = ctr ? fetch(lane) : gw;
     return cur;
@@ -273,6 +274,7 @@ struct TileSched {
     if (lane == 0) {
       v = atomicAdd(ctr, 1u);
       if (static_cast<long long>(v) == total + nwarps - 1) *ctr = 0u;
+      if (order && static_cast<long long>(v) < total) v = static_cast<unsigned long long>(__ldg(order + v));
     }
     return static_cast<long long>(__shfl_sync(0xffffffffu, v, 0));
   }
@@ -1239,7 +1241,7 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
   const BitCursor cur{p.res_cur, p.c, p.slot, p.W, p.n};
   const BitCursor prv{p.res_prev, p.c, p.slot, p.W, p.n};
 
-  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0};
+  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0, p.lt.order};  // boundary tiles first
   for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
@@ -1445,7 +1447,7 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
   const BitCursor cur{p.res_cur, p.c, p.slot, p.W, p.n};
-  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0};
+  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0, p.lt.order};  // boundary tiles first
   for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
@@ -1523,7 +1525,7 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0};
+  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0, p.lt.order};  // boundary tiles first
   for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
@@ -1705,7 +1707,7 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0};
+  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0, p.lt.order};  // boundary tiles first
   for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));

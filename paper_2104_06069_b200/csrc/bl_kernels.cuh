@@ -125,6 +125,7 @@ struct LayerTiles {
   const int* tile_layer;        // [tiles]
   const int* layer_tile_start;  // [L+1]
   unsigned int* ctr;            // dynamic tile counter (self-resetting) or nullptr
+  const int* order;             // [tiles] processing order (boundary tiles first) or nullptr
 };
 
 struct K5Params {

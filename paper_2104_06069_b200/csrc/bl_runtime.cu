@@ -671,8 +671,9 @@ void bl_cluster::sync_and_check(const std::vector<uint64_t>* off) {
 // bl_optimizer
 // ---------------------------------------------------------------------------
 bl::LayerTiles bl_optimizer::lt() const {
-  return {L, tiles, off_dev, tile_layer, layer_tile_start,
-          std::getenv("BL_STATIC_TILES") ? nullptr : cl->tile_ctr};
+  const bool dyn = std::getenv("BL_STATIC_TILES") == nullptr;
+  return {L, tiles, off_dev, tile_layer, layer_tile_start, dyn ? cl->tile_ctr : nullptr,
+          dyn ? tile_order : nullptr};
 }
 
 void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, bool adam) {
@@ -1431,6 +1432,24 @@ bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_
                      "k1 slow tiles");
       }
       o->tile_max = dalloc<float>(static_cast<size_t>(o->tiles));
+      {  // processing order of the layer-tiled kernels: boundary tiles (the
+         // per-row general path: misaligned layer start, partial tile, or a
+         // result-chunk boundary inside the tile) first, so their longer
+         // latency overlaps the bulk instead of forming the kernel's tail
+        std::vector<int> order, fast;
+        for (int l = 0; l < n_layers; ++l) {
+          const uint64_t lo = o->off[l], len = o->off[l + 1] - lo;
+          for (int t = tstart[l]; t < tstart[l + 1]; ++t) {
+            const uint64_t i = static_cast<uint64_t>(t - tstart[l]) * kTile, base = lo + i;
+            const bool f = (lo & 3u) == 0 && i + kTile <= len && base / cl->c == (base + kTile - 1) / cl->c;
+            (f ? fast : order).push_back(t);
+          }
+        }
+        order.insert(order.end(), fast.begin(), fast.end());
+        o->tile_order = reinterpret_cast<int*>(dalloc<float>(order.size()));
+        cuda_check(cudaMemcpy(o->tile_order, order.data(), order.size() * 4, cudaMemcpyHostToDevice),
+                   "tile order");
+      }
       std::vector<double> ones(L, 1.0);
       std::vector<float> onesf(L, 1.0f);
       cuda_check(cudaMemcpy(o->r_prev, ones.data(), L * 8, cudaMemcpyHostToDevice), "r_prev");
@@ -1453,7 +1472,7 @@ void bl_optimizer_destroy(bl_optimizer* o) {
   void* bufs[] = {o->off_dev, o->tile_layer, o->layer_tile_start, o->x, o->m, o->v, o->vf,
                   o->mprev, o->c_avg, o->r_prev, o->coeff, o->mag, o->A, o->B, o->invc, o->coef_x,
                   o->trace, o->cmean, o->es, o->counter, o->tile_sums, o->tile_max,
-                  o->k1_tile_layer, o->k1_slow};
+                  o->k1_tile_layer, o->k1_slow, o->tile_order};
   for (void* p : bufs)
     if (p) cudaFree(p);
   delete o;

@@ -165,6 +165,7 @@ struct bl_optimizer {
   uint64_t* off_dev = nullptr;
   int* tile_layer = nullptr;
   int* layer_tile_start = nullptr;
+  int* tile_order = nullptr;  // [tiles] boundary tiles first (LayerTiles::order)
   int tiles = 0;
   float *x = nullptr, *m = nullptr, *v = nullptr, *vf = nullptr, *mprev = nullptr;
   double *c_avg = nullptr, *r_prev = nullptr, *coeff = nullptr, *mag = nullptr;
