@@ -171,21 +171,6 @@ __device__ __forceinline__ uint32_t row_nibble(const uint32_t* words, int r, int
   return (__ldg(words + 4 * r + (lane >> 3)) >> (4 * (lane & 7))) & 0xFu;
 }
 
-// Pack the lane nibbles of one row into 4 packet words (LSB-first); with a
-// remote slot the word is also stored into the peer's memory over NVLink.
-__device__ __forceinline__ uint32_t store_row_bits(uint32_t* words, int r, int lane, uint32_t nib,
-                                                   uint32_t* remote = nullptr) {
-  uint32_t v = nib << (4 * (lane & 7));
-  v |= __shfl_xor_sync(FULL, v, 1);
-  v |= __shfl_xor_sync(FULL, v, 2);
-  v |= __shfl_xor_sync(FULL, v, 4);
-  if ((lane & 7) == 0) {
-    words[4 * r + (lane >> 3)] = v;
-    if (remote) remote[4 * r + (lane >> 3)] = v;
-  }
-  return v;
-}
-
 // Packet words of a tile are staged in a per-warp shared buffer (128 words)
 // and leave it once per tile as one 16-byte store per lane — locally and, for
 // the fused exchange, into peer HBM — instead of 4-byte stores per row.
@@ -568,7 +553,9 @@ __global__ void __launch_bounds__(kBlock, K1_MINB) k1_worker_compress(const K1Pa
                                       : (p.tile_cnt ? p.tile_cnt : per_w * p.nw);
   const float es = p.es_dev ? __ldg(p.es_dev) : p.es_host;
 
-  TileSched sch{p.slow_list ? nullptr : p.ctr, total, nwarps, 0};
+  // Boundary tiles first (order) when the whole index space is scheduled.
+  TileSched sch{p.slow_list ? nullptr : p.ctr, total, nwarps, 0,
+                p.slow_list || p.tile_cnt ? nullptr : p.order};
   for (long long it = sch.first(gw, lane); it < total; it = sch.next(lane)) {
     long long tile = it + p.tile_lo;
     if (p.slow_list) {  // iterate only the listed boundary tiles of every worker

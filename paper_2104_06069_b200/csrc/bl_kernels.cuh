@@ -68,6 +68,7 @@ struct K1Params {
   int n_slow;
   unsigned int* ctr;          // dynamic tile counter (self-resetting) or nullptr
   long long tile_lo, tile_cnt;  // register path: tiles [tile_lo, tile_lo + tile_cnt) (cnt 0: all)
+  const int* order;           // register path, all tiles: processing order (boundary first)
 };
 
 // K3: server reduction of chunk(s) owned locally.

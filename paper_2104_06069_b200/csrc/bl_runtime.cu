@@ -29,6 +29,24 @@ const char* const kClassNames[KC_COUNT] = {
 
 void fail(bl_status st, const std::string& msg) { throw Error{st, msg}; }
 
+int* boundary_first_order(const std::vector<int>& slow, int reps, int per) {
+  // Index space [reps][per]; the listed (per-rep) boundary tiles of every
+  // rep first, then the rest in order.  Scheduling only: results do not
+  // depend on it.
+  std::vector<char> is_slow(static_cast<size_t>(per), 0);
+  for (int t : slow) is_slow[static_cast<size_t>(t)] = 1;
+  std::vector<int> order;
+  order.reserve(static_cast<size_t>(reps) * per);
+  for (int r = 0; r < reps; ++r)
+    for (int t : slow) order.push_back(r * per + t);
+  for (int r = 0; r < reps; ++r)
+    for (int t = 0; t < per; ++t)
+      if (!is_slow[static_cast<size_t>(t)]) order.push_back(r * per + t);
+  int* d = reinterpret_cast<int*>(dalloc<float>(order.size()));
+  cuda_check(cudaMemcpy(d, order.data(), order.size() * 4, cudaMemcpyHostToDevice), "tile order");
+  return d;
+}
+
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(BL_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -149,6 +167,7 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
   if (!ovr) {
     p.slow_list = k1_slow;
     p.n_slow = k1_n_slow;
+    p.order = k1_order;
   }
   p.n = n;
   p.nw = nw;
@@ -780,6 +799,7 @@ void bl_optimizer::compressed_step(double lr) {
     p.tile_layer = k1_tile_layer;
     p.slow_list = k1_slow;
     p.n_slow = k1_n_slow;
+    p.order = k1_order;
     cl->verify_es_one = !hp.scaled_error_feedback;
     cl->compressed(&p, mode, 1.0f, es);
   }
@@ -1070,6 +1090,7 @@ bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
         if (!slow.empty())
           cuda_check(cudaMemcpy(c->k1_slow, slow.data(), slow.size() * 4, cudaMemcpyHostToDevice),
                      "k1 slow tiles");
+        c->k1_order = bl::boundary_first_order(slow, c->nw, c->n * c->tpc);
       }
       if (c->mode == BL_MODE_NCCL) {
         c->rpk = dalloc<uint32_t>(n * c->slot);
@@ -1100,7 +1121,7 @@ void bl_cluster_destroy(bl_cluster* c) {
                   c->scmax,     c->out,        c->lrecv,           c->err,       c->stat_part,
                   c->stat_max,  c->stat_out,   c->rx,              c->flags,     c->d_peer_rx,
                   c->d_peer_res, c->d_peer_flags, c->d_peer_in, c->d_peer_out, c->d_peer_err,
-                  c->lossless_done, c->small_bar, c->k1_slow, c->tile_ctr};
+                  c->lossless_done, c->small_bar, c->k1_slow, c->k1_order, c->tile_ctr};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& e : c->pending) {
@@ -1430,6 +1451,7 @@ bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_
         if (!slow.empty())
           cuda_check(cudaMemcpy(o->k1_slow, slow.data(), slow.size() * 4, cudaMemcpyHostToDevice),
                      "k1 slow tiles");
+        o->k1_order = bl::boundary_first_order(slow, cl->nw, cl->n * cl->tpc);
       }
       o->tile_max = dalloc<float>(static_cast<size_t>(o->tiles));
       {  // processing order of the layer-tiled kernels: boundary tiles (the
@@ -1472,7 +1494,7 @@ void bl_optimizer_destroy(bl_optimizer* o) {
   void* bufs[] = {o->off_dev, o->tile_layer, o->layer_tile_start, o->x, o->m, o->v, o->vf,
                   o->mprev, o->c_avg, o->r_prev, o->coeff, o->mag, o->A, o->B, o->invc, o->coef_x,
                   o->trace, o->cmean, o->es, o->counter, o->tile_sums, o->tile_max,
-                  o->k1_tile_layer, o->k1_slow, o->tile_order};
+                  o->k1_tile_layer, o->k1_slow, o->k1_order, o->tile_order};
   for (void* p : bufs)
     if (p) cudaFree(p);
   delete o;

@@ -50,6 +50,9 @@ extern const char* const kClassNames[KC_COUNT];
 template <typename T>
 T* dalloc(size_t n);  // zero-initialised device allocation
 
+// Device table over [reps][per] with the per-rep boundary tiles `slow` first.
+int* boundary_first_order(const std::vector<int>& slow, int reps, int per);
+
 }  // namespace bl
 
 struct bl_cluster {
@@ -101,6 +104,7 @@ struct bl_cluster {
   unsigned int* tile_ctr = nullptr;  // dynamic tile counter shared by the stream's kernels
   int* k1_slow = nullptr;       // API-mode K1 tiles that are not full/inside the data
   int k1_n_slow = 0;
+  int* k1_order = nullptr;      // API-mode K1 processing order, boundary tiles first
 
   // Host gradient staged for the next compressed collective: copied in
   // pieces that K1 consumes as they land (optimizer step, BL_MEM_HOST).
@@ -179,6 +183,7 @@ struct bl_optimizer {
   int* k1_tile_layer = nullptr;  // [n][tpc]: layer of a full single-layer K1 tile, else -1
   int* k1_slow = nullptr;        // the remaining (j*tpc+t) tiles
   int k1_n_slow = 0;
+  int* k1_order = nullptr;       // K1 processing order, boundary tiles first
   bool frozen = false, has_vf = false, has_mprev = false;
   bool m_valid = true;          // m buffer holds m (else: decompressed result * invc)
   bool mprev_separate = false;  // m_prev poked by the caller
