@@ -389,7 +389,9 @@ def main():
                        "mode": "nccl" if world > 1 else ("sim" if n > 1 else "single"),
                        "transport": cl.transport,
                        "parallelism": f"dp{cl.n_workers()}",
-                       "l2": "inputs larger than L2 (1.34 GB per state buffer vs 126 MB L2)"},
+                       "l2": (f"inputs larger than L2 ({4 * d / 1e9:.2f} GB per state buffer vs 126 MB L2)"
+                              if 4 * d > 126e6 else
+                              f"state buffers ({4 * d / 1e6:.0f} MB each) fit in the 126 MB L2; no flush")},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src,
