@@ -120,6 +120,66 @@ __device__ __forceinline__ float4 ldg_mis_ro(const float* p, int s) {
   return make_float4(ldg1_ro(p), m.x, m.y, ldg1_ro(p + 3));
 }
 
+// Read-write counterparts (plain .global path: the element is overwritten by
+// the same thread later in the kernel).  Inline PTX like the loads above, so
+// every access is issued exactly as written (naturally aligned pieces).
+__device__ __forceinline__ float2 ldg2_rw(const float* p) {
+  float2 v;
+  asm volatile("ld.global.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ldg1_rw(const float* p) {
+  float v;
+  asm volatile("ld.global.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stg2(float* p, float a, float b) {
+  asm volatile("st.global.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void stg1(float* p, float a) {
+  asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
+}
+__device__ __forceinline__ float4 ldg_mis_rw(const float* p, int s) {
+  if (s == 2) {
+    const float2 a = ldg2_rw(p), b = ldg2_rw(p + 2);
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  const float2 m = ldg2_rw(p + 1);
+  return make_float4(ldg1_rw(p), m.x, m.y, ldg1_rw(p + 3));
+}
+__device__ __forceinline__ void st_mis(float* p, int s, const float4& v) {
+  if (s == 2) {
+    stg2(p, v.x, v.y);
+    stg2(p + 2, v.z, v.w);
+    return;
+  }
+  stg1(p, v.x);
+  stg2(p + 1, v.y, v.z);
+  stg1(p + 3, v.w);
+}
+
+// Full-tile row batches of the layer-tiled kernels, for layers that start s
+// floats past a 16-byte boundary (MIS) or on one (s == 0): the same batch
+// code, instantiated twice, so a misaligned layer keeps the 4-row load
+// batches instead of the one-row-per-round-trip boundary path.
+template <bool B>
+struct Mis {
+  static constexpr bool value = B;
+};
+template <bool MIS>
+__device__ __forceinline__ float4 ld_ro_s(const float* p, int s) {
+  return MIS ? ldg_mis_ro(p, s) : ldg_ro(p);
+}
+template <bool MIS>
+__device__ __forceinline__ float4 ld_rw_s(const float* p, int s) {
+  return MIS ? ldg_mis_rw(p, s) : ldg_rw(p);
+}
+template <bool MIS>
+__device__ __forceinline__ void st_s(float* p, int s, const float4& v) {
+  if (MIS) st_mis(p, s, v);
+  else st4(p, v);
+}
+
 // R consecutive rows (row0 + k*128, k < R) of 4 elements per lane, row0 may be
 // misaligned by s floats.
 template <int R, bool RO>
@@ -1219,7 +1279,7 @@ __device__ __forceinline__ int lane_valid(uint64_t len, uint64_t ir, int lane) {
 #ifndef K5_MINB
 #define K5_MINB 3
 #endif
-template <int MPREV>
+template <int MPREV, bool MISK>
 __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p) {
   if (p.wait_flags) wait_peers(p.wait_flags, p.n, p.epoch, p.err);
   const int lane = threadIdx.x & 31;
@@ -1240,9 +1300,9 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
     uint64_t j = base / p.c, ce = (j + 1) * p.c;
     uint64_t jp = j, cep = ce;
 
-    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce && !p.dense &&
-        !p.norm_only) {
-      // Fast path: aligned, full tile, one chunk of the result.
+    if ((MISK || s == 0) && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce &&
+        !p.dense && !p.norm_only) {
+      // Fast path: full tile, one chunk of the result (MISK: any layer alignment).
       constexpr int R = K5_ROWS;
       const uint32_t* sl = cur.res + j * p.slot;
       const float S = slot_scale_cg(sl, p.W);
@@ -1258,37 +1318,46 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
       double acc = 0.0;
       float mx = 0.0f;
       bool bad = false;
-      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
-        float4 v[R], vf[R], mpb[R];
-        uint32_t nc[R], np[R];
+      auto rows = [&](auto mis) {
+        constexpr bool MIS = decltype(mis)::value;
+        for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+          float4 v[R], vf[R], mpb[R];
+          uint32_t nc[R], np[R];
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-          const float* row = p.v + base + (r0 + k) * kRowElems + 4 * lane;
-          v[k] = ldg_rw(row);
-          vf[k] = ldg_ro(p.vf + base + (r0 + k) * kRowElems + 4 * lane);
-          nc[k] = nibble_cg(sl, ib + (r0 + k) * kRowElems);
-          if (MPREV) np[k] = nibble_at(slp, ib + (r0 + k) * kRowElems);
-          else mpb[k] = ldg_ro(p.m + base + (r0 + k) * kRowElems + 4 * lane);
-        }
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          float4 vn;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float mg = __fmul_rn((nc[k] >> q) & 1u ? pos : neg, ic);
-            const float mp = MPREV ? __fmul_rn((np[k] >> q) & 1u ? posp : negp, ic) : comp(mpb[k], q);
-            const float rec = __fadd_rn(__fmul_rn(p.inv, mg), __fmul_rn(p.ninvb, mp));
-            const float nvv = __fadd_rn(__fmul_rn(p.b2, comp(v[k], q)),
-                                        __fmul_rn(__fmul_rn(p.omb2, rec), rec));
-            set_comp(vn, q, nvv);
-            bad |= !isfinite(rec);
-            const float den = nvv < p.floor_ ? p.floor_ : nvv;
-            const float ratio = fabsf(comp(vf[k], q)) / den;
-            mx = mx < ratio ? ratio : mx;
-            acc += static_cast<double>(nvv) * static_cast<double>(nvv);
+          for (int k = 0; k < R; ++k) {
+            const float* row = p.v + base + (r0 + k) * kRowElems + 4 * lane;
+            v[k] = ld_rw_s<MIS>(row, s);
+            vf[k] = ld_ro_s<MIS>(p.vf + base + (r0 + k) * kRowElems + 4 * lane, s);
+            nc[k] = nibble_cg(sl, ib + (r0 + k) * kRowElems);
+            if (MPREV) np[k] = nibble_at(slp, ib + (r0 + k) * kRowElems);
+            else mpb[k] = ld_ro_s<MIS>(p.m + base + (r0 + k) * kRowElems + 4 * lane, s);
           }
-          st4(p.v + base + (r0 + k) * kRowElems + 4 * lane, vn);
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            float4 vn;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float mg = __fmul_rn((nc[k] >> q) & 1u ? pos : neg, ic);
+              const float mp = MPREV ? __fmul_rn((np[k] >> q) & 1u ? posp : negp, ic) : comp(mpb[k], q);
+              const float rec = __fadd_rn(__fmul_rn(p.inv, mg), __fmul_rn(p.ninvb, mp));
+              const float nvv = __fadd_rn(__fmul_rn(p.b2, comp(v[k], q)),
+                                          __fmul_rn(__fmul_rn(p.omb2, rec), rec));
+              set_comp(vn, q, nvv);
+              bad |= !isfinite(rec);
+              const float den = nvv < p.floor_ ? p.floor_ : nvv;
+              const float ratio = fabsf(comp(vf[k], q)) / den;
+              mx = mx < ratio ? ratio : mx;
+              acc += static_cast<double>(nvv) * static_cast<double>(nvv);
+            }
+            st_s<MIS>(p.v + base + (r0 + k) * kRowElems + 4 * lane, s, vn);
+          }
         }
+      };
+      if constexpr (MISK) {
+        if (s != 0) rows(Mis<true>{});
+        else rows(Mis<false>{});
+      } else {
+        rows(Mis<false>{});
       }
       if (bad) flag(p.err, kErrRecon, static_cast<unsigned long long>(l));
       acc = warp_bfly_sum(acc);
@@ -1429,6 +1498,7 @@ __global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
 
 // K6 — update pass B (optimizers.cpp:308-313): u = m_g/(sqrt(vf)+eta) [+wd x],
 // x += (-lr*c)*u, with m_g recomputed from the result packets.
+template <bool MISK>
 __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1445,33 +1515,43 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
     const float ic = __ldg(p.invc + l);
     const float a = __ldg(p.coef_x + l);
     uint64_t j = base / p.c, ce = (j + 1) * p.c;
-    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce && !p.dense) {
+    if ((MISK || s == 0) && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce &&
+        !p.dense) {
       constexpr int R = 4;
       const uint32_t* sl = cur.res + j * p.slot;
       const float S = slot_scale(sl, p.W);
       const float pos = S, neg = S == 0.0f ? 0.0f : -S;
       const uint32_t ib = static_cast<uint32_t>(base - j * p.c) + 4 * lane;
-      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
-        float4 x[R], vf[R];
-        uint32_t nc[R];
+      auto rows = [&](auto mis) {
+        constexpr bool MIS = decltype(mis)::value;
+        for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+          float4 x[R], vf[R];
+          uint32_t nc[R];
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-          x[k] = ldg_rw(p.x + base + (r0 + k) * kRowElems + 4 * lane);
-          vf[k] = ldg_ro(p.vf + base + (r0 + k) * kRowElems + 4 * lane);
-          nc[k] = nibble_at(sl, ib + (r0 + k) * kRowElems);
-        }
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          float4 xn;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float mg = __fmul_rn((nc[k] >> q) & 1u ? pos : neg, ic);
-            float u = __fdiv_rn(mg, __fadd_rn(__fsqrt_rn(comp(vf[k], q)), p.eta));
-            if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
-            set_comp(xn, q, __fadd_rn(comp(x[k], q), __fmul_rn(a, u)));
+          for (int k = 0; k < R; ++k) {
+            x[k] = ld_rw_s<MIS>(p.x + base + (r0 + k) * kRowElems + 4 * lane, s);
+            vf[k] = ld_ro_s<MIS>(p.vf + base + (r0 + k) * kRowElems + 4 * lane, s);
+            nc[k] = nibble_at(sl, ib + (r0 + k) * kRowElems);
           }
-          st4(p.x + base + (r0 + k) * kRowElems + 4 * lane, xn);
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            float4 xn;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float mg = __fmul_rn((nc[k] >> q) & 1u ? pos : neg, ic);
+              float u = __fdiv_rn(mg, __fadd_rn(__fsqrt_rn(comp(vf[k], q)), p.eta));
+              if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
+              set_comp(xn, q, __fadd_rn(comp(x[k], q), __fmul_rn(a, u)));
+            }
+            st_s<MIS>(p.x + base + (r0 + k) * kRowElems + 4 * lane, s, xn);
+          }
         }
+      };
+      if constexpr (MISK) {
+        if (s != 0) rows(Mis<true>{});
+        else rows(Mis<false>{});
+      } else {
+        rows(Mis<false>{});
       }
       continue;
     }
@@ -1508,6 +1588,7 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
 // W1: m, v update; tile partials of ||x||^2 (pre-update), ||u||^2, ||v||^2 and
 // sum|m| (compute_scales, fusion.cpp:107-125, used when the stage ends).
 // ---------------------------------------------------------------------------
+template <bool MISK>
 __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1521,48 +1602,57 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
     const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
     const int s = static_cast<int>(lo & 3u);
     double ax = 0.0, au = 0.0, av = 0.0, am = 0.0;
-    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len) {
-      // Fast path: aligned full tile, 4 rows per batch, loads issued first.
-      constexpr int R = 4;
-      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
-        float4 g[R], m[R], v[R], x[R];
+    if ((MISK || s == 0) && static_cast<uint64_t>(t + 1) * kTile <= len) {
+      // Fast path: full tile, 4 rows per batch, loads issued first.
+      auto rows = [&](auto mis) {
+        constexpr bool MIS = decltype(mis)::value;
+        constexpr int R = 4;
+        for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+          float4 g[R], m[R], v[R], x[R];
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-          const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
-          g[k] = ldg_ro(p.gbar + o);
-          m[k] = ldg_rw(p.m + o);
-          v[k] = ldg_rw(p.v + o);
-          x[k] = ldg_ro(p.x + o);
-        }
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          if (p.err && !(isfinite(g[k].x) && isfinite(g[k].y) && isfinite(g[k].z) && isfinite(g[k].w))) {
-            for (int q = 0; q < 4; ++q)
-              if (!isfinite(comp(g[k], q)))
-                flag(p.err, kErrGrad, (static_cast<unsigned long long>(p.worker_base) << 40) |
-                                          (base + (r0 + k) * kRowElems + 4 * lane + q));
+          for (int k = 0; k < R; ++k) {
+            const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
+            g[k] = ld_ro_s<MIS>(p.gbar + o, s);
+            m[k] = ld_rw_s<MIS>(p.m + o, s);
+            v[k] = ld_rw_s<MIS>(p.v + o, s);
+            x[k] = ld_ro_s<MIS>(p.x + o, s);
           }
-          float4 mn, vn;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float gq = comp(g[k], q);
-            const float mq = __fadd_rn(__fmul_rn(p.b1, comp(m[k], q)), __fmul_rn(p.omb1, gq));
-            const float vq =
-                __fadd_rn(__fmul_rn(p.b2, comp(v[k], q)), __fmul_rn(__fmul_rn(p.omb2, gq), gq));
-            set_comp(mn, q, mq);
-            set_comp(vn, q, vq);
-            float u = __fdiv_rn(mq, __fadd_rn(__fsqrt_rn(vq), p.eta));
-            if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
-            const double xd = comp(x[k], q), ud = u, vd = vq;
-            ax += xd * xd;
-            au += ud * ud;
-            av += vd * vd;
-            am += fabs(static_cast<double>(mq));
+          for (int k = 0; k < R; ++k) {
+            if (p.err && !(isfinite(g[k].x) && isfinite(g[k].y) && isfinite(g[k].z) && isfinite(g[k].w))) {
+              for (int q = 0; q < 4; ++q)
+                if (!isfinite(comp(g[k], q)))
+                  flag(p.err, kErrGrad, (static_cast<unsigned long long>(p.worker_base) << 40) |
+                                            (base + (r0 + k) * kRowElems + 4 * lane + q));
+            }
+            float4 mn, vn;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float gq = comp(g[k], q);
+              const float mq = __fadd_rn(__fmul_rn(p.b1, comp(m[k], q)), __fmul_rn(p.omb1, gq));
+              const float vq =
+                  __fadd_rn(__fmul_rn(p.b2, comp(v[k], q)), __fmul_rn(__fmul_rn(p.omb2, gq), gq));
+              set_comp(mn, q, mq);
+              set_comp(vn, q, vq);
+              float u = __fdiv_rn(mq, __fadd_rn(__fsqrt_rn(vq), p.eta));
+              if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
+              const double xd = comp(x[k], q), ud = u, vd = vq;
+              ax += xd * xd;
+              au += ud * ud;
+              av += vd * vd;
+              am += fabs(static_cast<double>(mq));
+            }
+            const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
+            st_s<MIS>(p.m + o, s, mn);
+            st_s<MIS>(p.v + o, s, vn);
           }
-          const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
-          st4(p.m + o, mn);
-          st4(p.v + o, vn);
         }
+      };
+      if constexpr (MISK) {
+        if (s != 0) rows(Mis<true>{});
+        else rows(Mis<false>{});
+      } else {
+        rows(Mis<false>{});
       }
     } else
     for (int r = 0; r < kRowsPerTile; ++r) {
@@ -1690,6 +1780,7 @@ __global__ void __launch_bounds__(1024) k_wepilogue(const WEpiParams p) {
 }
 
 // W2: u = m/(sqrt(v)+eta) [+wd x]; x += (-lr*c)*u; at the freeze vf = v.
+template <bool MISK>
 __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1703,30 +1794,39 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
     const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
     const int s = static_cast<int>(lo & 3u);
     const float a = __ldg(p.coef_x + l);
-    if (s == 0 && static_cast<uint64_t>(t + 1) * kTile <= len) {
-      constexpr int R = 4;
-      for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
-        float4 m[R], v[R], x[R];
+    if ((MISK || s == 0) && static_cast<uint64_t>(t + 1) * kTile <= len) {
+      auto rows = [&](auto mis) {
+        constexpr bool MIS = decltype(mis)::value;
+        constexpr int R = 4;
+        for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+          float4 m[R], v[R], x[R];
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-          const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
-          m[k] = ldg_ro(p.m + o);
-          v[k] = ldg_ro(p.v + o);
-          x[k] = ldg_rw(p.x + o);
-        }
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          float4 xn;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float u = __fdiv_rn(comp(m[k], q), __fadd_rn(__fsqrt_rn(comp(v[k], q)), p.eta));
-            if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
-            set_comp(xn, q, __fadd_rn(comp(x[k], q), __fmul_rn(a, u)));
+          for (int k = 0; k < R; ++k) {
+            const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
+            m[k] = ld_ro_s<MIS>(p.m + o, s);
+            v[k] = ld_ro_s<MIS>(p.v + o, s);
+            x[k] = ld_rw_s<MIS>(p.x + o, s);
           }
-          const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
-          st4(p.x + o, xn);
-          if (p.finalize) st4(p.vf + o, v[k]);  // optimizers.cpp:205
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            float4 xn;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float u = __fdiv_rn(comp(m[k], q), __fadd_rn(__fsqrt_rn(comp(v[k], q)), p.eta));
+              if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
+              set_comp(xn, q, __fadd_rn(comp(x[k], q), __fmul_rn(a, u)));
+            }
+            const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
+            st_s<MIS>(p.x + o, s, xn);
+            if (p.finalize) st_s<MIS>(p.vf + o, s, v[k]);  // optimizers.cpp:205
+          }
         }
+      };
+      if constexpr (MISK) {
+        if (s != 0) rows(Mis<true>{});
+        else rows(Mis<false>{});
+      } else {
+        rows(Mis<false>{});
       }
       continue;
     }
@@ -2423,7 +2523,8 @@ bool k1_uses_bulk(const K1Params& p, int mode) {
   // Only odd chunk lengths (4-byte-aligned chunk starts) go through the bulk
   // pipeline; 8-byte-aligned chunks load as float2 on the register path,
   // which measures faster there (BERT-L sim2: 1.35 vs 1.42 ms).
-  const bool misaligned = (p.c & 1u) != 0;
+  // A single chunk (n == 1) starts at element 0 and is always aligned.
+  const bool misaligned = (p.c & 1u) != 0 && p.n > 1;
   return mode != 1 && (mode == 0 || p.tile_layer) && (misaligned || bulk_all()) && !bulk_none();
 }
 
@@ -2450,7 +2551,7 @@ int launch_k1(const K1Params& p, int mode, int grid, cudaStream_t s) {
   full.n_slow = 0;
   full.skip_fast = 0;
 #define BL_K1(M, A) k1_worker_compress<M, A><<<resident(k1_worker_compress<M, A>, grid), kBlock, 0, s>>>(full)
-  const bool al = (p.c & 3u) == 0;  // every chunk start 16-byte aligned
+  const bool al = (p.c & 3u) == 0 || p.n == 1;  // every chunk start 16-byte aligned
   switch (mode) {
     case 0: if (al) BL_K1(0, true); else BL_K1(0, false); break;
     case 1: BL_K1(1, false); break;
@@ -2477,8 +2578,13 @@ int launch_k3(const K3Params& p, int grid, cudaStream_t s) {
 }
 
 int launch_k5(const K5Params& p, int grid, cudaStream_t s) {
-  if (p.res_prev) k5_update_a<1><<<resident(k5_update_a<1>, grid), kBlock, 0, s>>>(p);
-  else k5_update_a<0><<<resident(k5_update_a<0>, grid), kBlock, 0, s>>>(p);
+#define BL_K5(M, X) k5_update_a<M, X><<<resident(k5_update_a<M, X>, grid), kBlock, 0, s>>>(p)
+  if (p.res_prev) {
+    if (p.lt.mis) BL_K5(1, true); else BL_K5(1, false);
+  } else {
+    if (p.lt.mis) BL_K5(0, true); else BL_K5(0, false);
+  }
+#undef BL_K5
   return 1;
 }
 
@@ -2488,12 +2594,14 @@ int launch_epilogue(const EpiParams& p, cudaStream_t s) {
 }
 
 int launch_k6(const K6Params& p, int grid, cudaStream_t s) {
-  k6_update_b<<<resident(k6_update_b, grid), kBlock, 0, s>>>(p);
+  if (p.lt.mis) k6_update_b<true><<<resident(k6_update_b<true>, grid), kBlock, 0, s>>>(p);
+  else k6_update_b<false><<<resident(k6_update_b<false>, grid), kBlock, 0, s>>>(p);
   return 1;
 }
 
 int launch_w1(const W1Params& p, int grid, cudaStream_t s) {
-  kw1_warmup_a<<<resident(kw1_warmup_a, grid), kBlock, 0, s>>>(p);
+  if (p.lt.mis) kw1_warmup_a<true><<<resident(kw1_warmup_a<true>, grid), kBlock, 0, s>>>(p);
+  else kw1_warmup_a<false><<<resident(kw1_warmup_a<false>, grid), kBlock, 0, s>>>(p);
   return 1;
 }
 
@@ -2503,7 +2611,8 @@ int launch_wepilogue(const WEpiParams& p, cudaStream_t s) {
 }
 
 int launch_w2(const W2Params& p, int grid, cudaStream_t s) {
-  kw2_warmup_b<<<resident(kw2_warmup_b, grid), kBlock, 0, s>>>(p);
+  if (p.lt.mis) kw2_warmup_b<true><<<resident(kw2_warmup_b<true>, grid), kBlock, 0, s>>>(p);
+  else kw2_warmup_b<false><<<resident(kw2_warmup_b<false>, grid), kBlock, 0, s>>>(p);
   return 1;
 }
 

@@ -127,6 +127,7 @@ struct LayerTiles {
   const int* layer_tile_start;  // [L+1]
   unsigned int* ctr;            // dynamic tile counter (self-resetting) or nullptr
   const int* order;             // [tiles] processing order (boundary tiles first) or nullptr
+  int mis;                      // some full tile lies in a layer not 16-B aligned
 };
 
 struct K5Params {

@@ -692,7 +692,7 @@ void bl_cluster::sync_and_check(const std::vector<uint64_t>* off) {
 bl::LayerTiles bl_optimizer::lt() const {
   const bool dyn = std::getenv("BL_STATIC_TILES") == nullptr;
   return {L, tiles, off_dev, tile_layer, layer_tile_start, dyn ? cl->tile_ctr : nullptr,
-          dyn ? tile_order : nullptr};
+          dyn ? tile_order : nullptr, mis_layers ? 1 : 0};
 }
 
 void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, bool adam) {
@@ -1458,12 +1458,17 @@ bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_
          // per-row general path: misaligned layer start, partial tile, or a
          // result-chunk boundary inside the tile) first, so their longer
          // latency overlaps the bulk instead of forming the kernel's tail
+        // A layer of at least one full tile that starts off a 16-byte
+        // boundary selects the kernels' misaligned full-tile path (LayerTiles::mis).
+        for (int l = 0; l < n_layers; ++l)
+          if ((o->off[l] & 3u) != 0 && o->off[l + 1] - o->off[l] >= kTile) o->mis_layers = true;
         std::vector<int> order, fast;
         for (int l = 0; l < n_layers; ++l) {
           const uint64_t lo = o->off[l], len = o->off[l + 1] - lo;
           for (int t = tstart[l]; t < tstart[l + 1]; ++t) {
             const uint64_t i = static_cast<uint64_t>(t - tstart[l]) * kTile, base = lo + i;
-            const bool f = (lo & 3u) == 0 && i + kTile <= len && base / cl->c == (base + kTile - 1) / cl->c;
+            const bool f = ((lo & 3u) == 0 || o->mis_layers) && i + kTile <= len &&
+                           base / cl->c == (base + kTile - 1) / cl->c;
             (f ? fast : order).push_back(t);
           }
         }

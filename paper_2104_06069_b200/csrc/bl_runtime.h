@@ -170,6 +170,7 @@ struct bl_optimizer {
   int* tile_layer = nullptr;
   int* layer_tile_start = nullptr;
   int* tile_order = nullptr;  // [tiles] boundary tiles first (LayerTiles::order)
+  bool mis_layers = false;    // a layer of >= one tile starts off a 16-B boundary
   int tiles = 0;
   float *x = nullptr, *m = nullptr, *v = nullptr, *vf = nullptr, *mprev = nullptr;
   double *c_avg = nullptr, *r_prev = nullptr, *coeff = nullptr, *mag = nullptr;

@@ -476,3 +476,13 @@ def test_device_resident_step_matches_host_step(bl):
             opt.step(torch.from_numpy(g).cuda() if dev else g, t, 1e-3, trace=t == 7)
         res.append(opt.get("x"))
     assert_same(res[0], res[1])
+
+
+@pytest.mark.parametrize("lead", [1, 2, 3])
+@pytest.mark.parametrize("n", [1, 2])
+@pytest.mark.parametrize("variant", ["onebit_lamb", "lamb_basic_1bit", "lamb"])
+def test_misaligned_layer_full_tiles_bitexact(bl, lead, n, variant):
+    """A layer of full tiles starting 1-3 floats past a 16-byte boundary takes
+    the kernels' misaligned full-tile path (W1/W2/K5/K6); bit-exact with the
+    f32 oracle like the aligned and per-row paths."""
+    run_pair(bl, [lead, 3 * 4096 + 5, 7, 4096], n, steps=8, warmup=3, seed=40 + lead, variant=variant)
