@@ -11,9 +11,11 @@ K1 worker compress -> alltoall -> K3 server reduce -> allgather -> K5/K6
 update.  `value` times K steps on device-resident gradients with CUDA events
 on the library's stream (max over ranks); `e2e` times the same step through
 the C-ABI with the gradient in pinned HOST memory (H2D copy + trace D2H inside
-the timed region).  The reference arm runs the reference library
-(oracle/_ref, fp64, OpenMP) on the host cores on a bounded sample of the same
-layout and extrapolates per parameter.
+the timed region).  The reference arm runs the reference library itself
+(oracle/_ref: the unmodified reference sources, fp64, OpenMP over every host
+core) on the SAME full layout and worker count; it times as many of the
+requested steps as fit a bounded budget and reports the steps it timed.
+Both arms print the identical `config` object.
 """
 from __future__ import annotations
 
@@ -133,57 +135,71 @@ def algorithmic_bytes(d: int, n: int, nw: int) -> dict:
 # ---------------------------------------------------------------------------
 # reference arm / cpu baseline: the reference library on the host cores
 # ---------------------------------------------------------------------------
-def reference_sample(layout, n: int, target_params: int = 12_000_000, steps: int = 3):
-    """Time the reference's compression-stage Optimizer::step (oracle/_ref,
-    fp64, OpenMP over all host cores) on the leading tensors of `layout`
-    holding ~target_params parameters; returns seconds per step and the sample."""
-    from oracle import oracle as O
-
-    sizes, tot = [], 0
-    for _, s in layout:
-        if tot + s > target_params and sizes:
-            # take a slice of the next tensor so the sample hits the target
-            rest = target_params - tot
-            if rest > 1024:
-                sizes.append(rest)
-                tot += rest
-            break
-        sizes.append(s)
-        tot += s
-    d = tot
-    hp = O.HyperParams(total_steps=steps + 2, warmup_steps=1)
-    cl = O.Cluster("ref", n, d)
-    opt = O.Optimizer("ref", "onebit_lamb", sizes, hp)
-    rng = np.random.default_rng(1)
-    opt.set("x", rng.standard_normal(d) * 0.02)
-    sig = np.repeat(grad_sigma(sizes), sizes)
-    g = rng.standard_normal((n, d)) * sig
-    opt.step(g, 0, 1e-3, cl)  # warmup LAMB + freeze
-    opt.step(g, 1, 1e-3, cl)  # first compression step (untimed)
-    times = []
-    for t in range(steps):
-        t0 = time.perf_counter()
-        opt.step(g, 2 + t, 1e-3, cl)
-        times.append(time.perf_counter() - t0)
-    return float(np.median(times)), d, len(sizes)
-
-
 def cpu_cores() -> int:
     """Host threads given to the reference: BL_REF_THREADS, else every core
     (torchrun exports OMP_NUM_THREADS=1, which must not throttle the baseline)."""
     return int(os.environ.get("BL_REF_THREADS", os.cpu_count() or 1))
 
 
-def run_reference(args, layout, d_full: int, n: int) -> dict:
+def reference_run(layout, n: int, steps: int, warmup: int, budget_s: float) -> dict:
+    """The reference's own compression-stage Optimizer::step (optimizers.cpp:
+    334-364; oracle/_ref = the unmodified reference sources, fp64, OpenMP over
+    the host cores) on the FULL layout with n simulated workers.
+
+    Warm start: one warmup LAMB step that freezes (T_w = 1), then up to
+    `warmup` untimed compression steps, then up to `steps` timed ones.  Each
+    step is timed in C++ around the stock call alone (gradients already in the
+    reference's [worker][layer] form, as our arm's are resident in HBM).  The
+    timed steps stop early once their total would pass `budget_s`; the line
+    reports the steps actually timed."""
     from oracle import oracle as O
 
+    sizes = layouts.sizes(layout)
+    d = sum(sizes)
     cores = O.set_reference_threads(cpu_cores())
-    s, d_s, L_s = reference_sample(layout, n, steps=max(1, min(args.steps, 3)))
-    ms = s * 1e3 * d_full / d_s
-    sample = (f"reference Optimizer::step (compression stage, n={n} simulated workers) on the "
-              f"first {L_s} BERT-Large tensors ({d_s:,} params), median of "
-              f"{max(1, min(args.steps, 3))} steps, extrapolated x{d_full / d_s:.2f} by parameter count")
-    return {"value": ms, "unit": "ms", "cores": cores, "kind": "reference", "sample": sample}
+    rng = np.random.default_rng(1)
+    hp = O.HyperParams(total_steps=2 + warmup + steps, warmup_steps=1)
+    cl = O.Cluster("ref", n, d)
+    opt = O.Optimizer("ref", "onebit_lamb", sizes, hp)
+    opt.set("x", rng.standard_normal(d, dtype=np.float32) * np.float32(0.02))
+    sig = np.repeat(grad_sigma(sizes), sizes).astype(np.float32)
+    g = np.empty((n, d), dtype=np.float64)
+    for i in range(n):
+        g[i] = rng.standard_normal(d, dtype=np.float32) * sig
+    del sig
+    opt.load_grads(g)
+    del g
+    lr = 1e-3
+    opt.step_loaded(0, lr, cl)  # warmup LAMB + finalize_warmup (freeze)
+    t, warm_done = 1, 0
+    for _ in range(max(0, warmup)):
+        opt.step_loaded(t, lr, cl)
+        t, warm_done = t + 1, warm_done + 1
+    times = []
+    while len(times) < max(1, steps):
+        sec, comp = opt.step_loaded(t, lr, cl)
+        assert comp, "reference step did not run the compression stage"
+        times.append(sec)
+        t += 1
+        if sum(times) + sum(times) / len(times) > budget_s:
+            break
+    ms = 1e3 * sum(times) / len(times)
+    sample = (f"reference Optimizer::step, compression stage, full layout ({d:,} params, "
+              f"{len(sizes)} tensors), {n} simulated worker(s); {len(times)} timed step(s) "
+              f"(mean; requested {steps}) after 1 warmup LAMB step + freeze and {warm_done} untimed "
+              f"compression step(s); {cores} OpenMP threads")
+    return {"value": ms, "unit": "ms", "cores": cores, "kind": "reference", "sample": sample,
+            "steps_timed": len(times), "warmup_done": 1 + warm_done,
+            "step_ms": [1e3 * x for x in times]}
+
+
+def workload_config(args, d: int, n_layers: int, world: int) -> dict:
+    """The `config` object both arms print (identical by construction)."""
+    return {"workload": f"{args.workload} 1-bit LAMB {args.stage}-stage step",
+            "params": d, "layers": n_layers, "world": world, "parallelism": f"dp{world}",
+            "l2": (f"inputs larger than L2 ({4 * d / 1e9:.2f} GB per state buffer vs 126 MB L2)"
+                   if 4 * d > 126e6 else
+                   f"state buffers ({4 * d / 1e6:.0f} MB each) fit in the 126 MB L2; no flush")}
 
 
 # ---------------------------------------------------------------------------
@@ -199,6 +215,8 @@ def main():
     ap.add_argument("--sim-workers", type=int, default=0,
                     help="simulate this many ranks on one GPU instead of one rank per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="reference arm: stop timing steps once their total passes this many seconds")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
                     help="NCCL-mode packet exchange: fused NVLink peer stores or NCCL")
@@ -221,19 +239,23 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        ref = run_reference(args, layout, d, n)
+        if args.stage != "compression":
+            print(json.dumps({"impl": "reference", "unavailable": "reference arm times the compression stage"}))
+            return
+        ref = reference_run(layout, n, args.steps, min(args.warmup, 1), budget_s=args.ref_budget)
         line = {"impl": "reference",
                 "metric": METRIC if args.workload == "bert-large" else f"1-bit LAMB step time, {args.workload}",
                 "value": ref["value"], "unit": "ms",
-                "n_gpus": args.gpus if world == 1 else world, "steps": args.steps, "warmup": args.warmup,
+                "n_gpus": args.gpus if world == 1 else world,
+                # the steps actually timed / run untimed (requested: steps_requested, warmup_requested)
+                "steps": ref["steps_timed"], "warmup": ref["warmup_done"],
+                "steps_requested": args.steps, "warmup_requested": args.warmup,
                 "ms_per_step": ref["value"], "higher_is_better": False, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                # the same workload as our arm's line; the reference runs its
-                # n data-parallel workers as simulated workers on the host
-                "config": {"workload": f"{args.workload} 1-bit LAMB compression-stage step",
-                           "params": d, "layers": len(sizes), "world": n,
-                           "mode": "reference CPU, simulated workers", "parallelism": f"dp{n}"},
-                "cpu_baseline": ref,
+                "config": workload_config(args, d, len(sizes), n),
+                "placement": {"mode": "reference CPU library, simulated workers", "cores": ref["cores"]},
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "step_ms": ref["step_ms"],
                 "e2e": {"value": ref["value"], "unit": "ms", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -370,9 +392,10 @@ def main():
     del grads
     torch.cuda.empty_cache()
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = run_reference(args, layout, d, cl.n_workers())
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.stage == "compression":
+        try:  # one timed reference step on the same full layout (bounded: ~1 min of CPU work)
+            ref = reference_run(layout, cl.n_workers(), 1, 1, budget_s=0.0)
+            cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as exc:  # reported, never silently replaced
             cpu = {"error": f"{type(exc).__name__}: {exc}"}
 
@@ -384,14 +407,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.workload} 1-bit LAMB compression-stage step",
-                       "params": d, "layers": len(sizes), "world": cl.n_workers(),
-                       "mode": "nccl" if world > 1 else ("sim" if n > 1 else "single"),
-                       "transport": cl.transport,
-                       "parallelism": f"dp{cl.n_workers()}",
-                       "l2": (f"inputs larger than L2 ({4 * d / 1e9:.2f} GB per state buffer vs 126 MB L2)"
-                              if 4 * d > 126e6 else
-                              f"state buffers ({4 * d / 1e6:.0f} MB each) fit in the 126 MB L2; no flush")},
+            "config": workload_config(args, d, len(sizes), cl.n_workers()),
+            "placement": {"mode": "nccl" if world > 1 else ("sim" if n > 1 else "single"),
+                          "transport": cl.transport},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src,

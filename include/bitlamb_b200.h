@@ -152,6 +152,10 @@ void bl_cluster_destroy(bl_cluster* c);
 bl_status bl_cluster_dims(const bl_cluster* c, uint64_t* padded, uint64_t* chunk);
 /* The packet transport in use (bl_transport; BL_TRANSPORT_AUTO is resolved). */
 int32_t bl_cluster_transport(const bl_cluster* c);
+/* The CUDA stream (cudaStream_t) every device call of this cluster and of its
+ * optimizer is enqueued on.  Callers that produce inputs on another stream
+ * make this stream wait on theirs (and theirs on this one for outputs). */
+void* bl_cluster_stream(const bl_cluster* c);
 
 /* SimCluster::compressed_allreduce (comm_sim.hpp:98-99, comm_sim.cpp:120-203).
  * inputs[i] is worker i's stream of `len` floats (len must equal dim,

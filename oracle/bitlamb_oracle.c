@@ -26,7 +26,43 @@
 #define OC_FABS(x) fabs(x)
 #endif
 
+/* OpenMP: elementwise maps and per-tile / per-block partial sums run in
+ * parallel; every reduction still combines its partials in the canonical
+ * order (serially), so results are independent of the thread count.  Small
+ * vectors stay serial. */
+#ifdef _OPENMP
+#define OC_PAR _Pragma("omp parallel for schedule(static) if (n_ > 65536)")
+#else
+#define OC_PAR
+#endif
+
 static _Thread_local char g_err[512];
+
+/* Reusable scratch (grow-only, one buffer per role) and parallel copies: at
+ * BERT-Large sizes fresh 1.3 GB allocations and serial memcpy dominated the
+ * checker's run time.  Roles never nest with themselves. */
+enum { S_PAD, S_CORR, S_DEC, S_WBITS, S_INBOX, S_AVG, S_CORR2, S_DEC2, S_SBITS, S_RESULT, S_STREAMS,
+       S_MG, S_REC, S_U, S_LAVG, S_COUNT };
+static void* g_scr[S_COUNT];
+static size_t g_scr_n[S_COUNT];
+static void* scratch(int role, size_t bytes) {
+  if (bytes + 64u > g_scr_n[role]) {
+    free(g_scr[role]);
+    g_scr[role] = malloc(bytes + 64u);
+    g_scr_n[role] = bytes + 64u;
+  }
+  return g_scr[role];
+}
+static void pcopy(void* dst, const void* src, size_t bytes) {
+  const size_t blk = (size_t)1 << 22, nb = (bytes + blk - 1u) / blk;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) if (nb > 4)
+#endif
+  for (size_t b = 0; b < nb; ++b) {
+    const size_t o = b * blk, k = bytes - o < blk ? bytes - o : blk;
+    memcpy((char*)dst + o, (const char*)src + o, k);
+  }
+}
 
 static int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -71,6 +107,13 @@ static double tile_partial(const oc_real* x, uint64_t len, uint64_t t, int kind)
   double acc[32];
   for (int l = 0; l < 32; ++l) acc[l] = 0.0;
   const uint64_t base = t * 4096u;
+  if (base + 4096u <= len) { /* full tile: same order, no bounds test */
+    const oc_real* xt = x + base;
+    for (int r = 0; r < 32; ++r)
+      for (int l = 0; l < 32; ++l)
+        for (int q = 0; q < 4; ++q) acc[l] += term(xt[128 * r + 4 * l + q], kind);
+    return butterfly32(acc);
+  }
   for (int r = 0; r < 32; ++r) {
     for (int l = 0; l < 32; ++l) {
       for (int q = 0; q < 4; ++q) {
@@ -95,6 +138,8 @@ static double canonical_sum(const oc_real* x, uint64_t len, int kind) {
   const uint64_t T = (len + 4095u) / 4096u;
   if (T == 0) return 0.0;
   double* p = malloc(T * sizeof(double));
+  const uint64_t n_ = len;
+  OC_PAR
   for (uint64_t t = 0; t < T; ++t) p[t] = tile_partial(x, len, t, kind);
   const double s = combine_partials(p, T);
   free(p);
@@ -111,13 +156,17 @@ static double serial_sum(const oc_real* x, uint64_t lo, uint64_t hi, int kind) {
 
 static double canonical_sum(const oc_real* x, uint64_t len, int kind) {
   if (len <= 4096u) return serial_sum(x, 0, len, kind);
-  const uint64_t nb = (len + 4095u) / 4096u;
-  double acc = 0.0;
+  const uint64_t nb = (len + 4095u) / 4096u, n_ = len;
+  double* part = malloc(nb * sizeof(double));
+  OC_PAR
   for (uint64_t b = 0; b < nb; ++b) {
     const uint64_t lo = b * 4096u;
     const uint64_t hi = lo + 4096u < len ? lo + 4096u : len;
-    acc += serial_sum(x, lo, hi, kind);
+    part[b] = serial_sum(x, lo, hi, kind);
   }
+  double acc = 0.0;
+  for (uint64_t b = 0; b < nb; ++b) acc += part[b]; /* block partials in order */
+  free(part);
   return acc;
 }
 #endif
@@ -131,10 +180,24 @@ static double max_abs_ratio(const oc_real* a, const oc_real* b, uint64_t n,
                             double floor_) {
   const oc_real fl = R(floor_);
   oc_real m = 0;
-  for (uint64_t i = 0; i < n; ++i) {
-    const oc_real den = b[i] < fl ? fl : b[i]; /* std::max(b[i], floor) */
-    const oc_real q = OC_FABS(a[i]) / den;
-    m = m < q ? q : m; /* std::max(m, q) */
+  const uint64_t n_ = n;
+#ifdef _OPENMP
+#pragma omp parallel if (n_ > 65536)
+#endif
+  {
+    oc_real mt = 0; /* maxima are order-free: per-thread, then combined by the same rule */
+#ifdef _OPENMP
+#pragma omp for schedule(static) nowait
+#endif
+    for (uint64_t i = 0; i < n; ++i) {
+      const oc_real den = b[i] < fl ? fl : b[i]; /* std::max(b[i], floor) */
+      const oc_real q = OC_FABS(a[i]) / den;
+      mt = mt < q ? q : mt; /* std::max(m, q) */
+    }
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+    m = m < mt ? mt : m;
   }
   return (double)m;
 }
@@ -142,17 +205,35 @@ static double max_abs_ratio(const oc_real* a, const oc_real* b, uint64_t n,
 /* kernels.cpp:172-183 max_abs */
 static double max_abs(const oc_real* v, uint64_t n) {
   oc_real m = 0;
-  for (uint64_t i = 0; i < n; ++i) {
-    const oc_real a = OC_FABS(v[i]);
-    m = m < a ? a : m; /* std::max(m, std::abs(x)) */
+  const uint64_t n_ = n;
+#ifdef _OPENMP
+#pragma omp parallel if (n_ > 65536)
+#endif
+  {
+    oc_real mt = 0;
+#ifdef _OPENMP
+#pragma omp for schedule(static) nowait
+#endif
+    for (uint64_t i = 0; i < n; ++i) {
+      const oc_real a = OC_FABS(v[i]);
+      mt = mt < a ? a : mt; /* std::max(m, std::abs(x)) */
+    }
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+    m = m < mt ? mt : m;
   }
   return (double)m;
 }
 
 static int all_finite(const oc_real* v, uint64_t n) {
-  for (uint64_t i = 0; i < n; ++i)
-    if (!oc_isfinite(v[i])) return 0;
-  return 1;
+  int ok = 1;
+  const uint64_t n_ = n;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) reduction(&& : ok) if (n_ > 65536)
+#endif
+  for (uint64_t i = 0; i < n; ++i) ok = ok && oc_isfinite(v[i]);
+  return ok;
 }
 
 /* vector_ops.cpp:25-28 */
@@ -174,9 +255,13 @@ typedef struct {
 /* compression.cpp:37-60 CompressedBlock::compress */
 static int block_compress(const oc_real* v, uint64_t len, oc_block* b) {
   b->len = len;
-  memset(b->bits, 0, (len + 7u) / 8u);
-  for (uint64_t i = 0; i < len; ++i) {
-    if (v[i] >= 0) b->bits[i >> 3] |= (uint8_t)(1u << (i & 7u));
+  const uint64_t nbytes = (len + 7u) / 8u, n_ = len;
+  OC_PAR
+  for (uint64_t y = 0; y < nbytes; ++y) { /* byte-parallel, as compression.cpp:42-53 */
+    uint8_t byte = 0;
+    for (uint64_t i = 8u * y; i < 8u * y + 8u && i < len; ++i)
+      if (v[i] >= 0) byte |= (uint8_t)(1u << (i & 7u));
+    b->bits[y] = byte;
   }
   const double s = len == 0 ? 0.0 : canonical_sum(v, len, SUM_ABS) / (double)len;
   b->scale = R(s);
@@ -190,6 +275,8 @@ static int bit_at(const uint8_t* bits, uint64_t i) { return (bits[i >> 3] >> (i 
 
 /* compression.cpp:68-81 decompress_into */
 static void block_decompress(const uint8_t* bits, oc_real s, uint64_t len, oc_real* out) {
+  const uint64_t n_ = len;
+  OC_PAR
   for (uint64_t i = 0; i < len; ++i) out[i] = s == 0 ? (oc_real)0 : (bit_at(bits, i) ? s : -s);
 }
 
@@ -234,6 +321,8 @@ static void stored_to_wire(const uint8_t* pkt, uint64_t len, uint8_t* out) {
 static int compress_with_feedback(const oc_real* v, oc_real* delta, uint64_t len, int kind,
                                   double es, oc_real* corrected, oc_block* out) {
   const oc_real a = R(1.0), b = R(es);
+  const uint64_t n_ = len;
+  OC_PAR
   for (uint64_t i = 0; i < len; ++i) corrected[i] = a * v[i] + b * delta[i]; /* :181 */
   if (kind == 1) {                                                           /* :184-188 */
     for (uint64_t i = 0; i < len; ++i) delta[i] = 0;
@@ -244,6 +333,7 @@ static int compress_with_feedback(const oc_real* v, oc_real* delta, uint64_t len
   int st = block_compress(corrected, len, out); /* :182 */
   if (st) return st;
   const oc_real s = out->scale;
+  OC_PAR
   for (uint64_t i = 0; i < len; ++i) { /* :190-196 */
     const oc_real rec = bit_at(out->bits, i) ? s : -s;
     delta[i] = v[i] + delta[i] - rec;
@@ -298,7 +388,7 @@ typedef struct {
   uint64_t dim, padded, chunk;
   oc_real* werr;      /* n x padded   (:60) */
   oc_real* serr;      /* n x chunk    (:61) */
-  oc_real* wcorr;     /* n x padded   (:62) */
+  double* wcmax;      /* n: max|corrected| of worker_corrected_ (:62), kept as its maximum only */
   uint8_t* wpk;       /* [worker][server] serialized packets of the last call */
   uint8_t* spk;       /* [server] serialized server packets of the last call */
   oc_stats* wstats;   /* n */
@@ -323,7 +413,7 @@ int oc_cluster_new(int n, uint64_t dim, int kind, int baseline_bits, int verify,
   c->chunk = c->padded / (uint64_t)n;
   c->werr = calloc((size_t)n * c->padded, sizeof(oc_real));
   c->serr = calloc((size_t)n * c->chunk, sizeof(oc_real));
-  c->wcorr = calloc((size_t)n * c->padded, sizeof(oc_real));
+  c->wcmax = calloc((size_t)n, sizeof(double));
   c->wpk = calloc((size_t)n * (size_t)n * ipkt_bytes(c->chunk), 1);
   c->spk = calloc((size_t)n * ipkt_bytes(c->chunk), 1);
   c->wstats = calloc((size_t)n, sizeof(oc_stats));
@@ -339,7 +429,7 @@ void oc_cluster_free(void* cv) {
   if (!c) return;
   free(c->werr);
   free(c->serr);
-  free(c->wcorr);
+  free(c->wcmax);
   free(c->wpk);
   free(c->spk);
   free(c->wstats);
@@ -393,33 +483,37 @@ static void stats_update(oc_stats* s, double l2, double linf, double cinf) {
 
 /* Worker phase of comm_sim.cpp:133-149 for one worker: padded copy, then every
  * chunk compressed with its slice of the worker residual.  packets: n slots of
- * ipkt_bytes(chunk) (in-memory layout).  corr_out: padded scratch (may be NULL). */
+ * ipkt_bytes(chunk) (in-memory layout).  corr_max (may be NULL) receives
+ * max|corrected| over the padded stream (the endpoint statistic of :108-118). */
 static int worker_phase(const oc_real* input, uint64_t dim, int n, int kind, oc_real* werr,
-                        double es, uint8_t* packets, oc_real* corr_out, const oc_cluster* vc) {
+                        double es, uint8_t* packets, double* corr_max, const oc_cluster* vc) {
   const uint64_t padded = (dim + (uint64_t)n - 1u) / (uint64_t)n * (uint64_t)n;
   const uint64_t chunk = padded / (uint64_t)n;
-  oc_real* p = calloc(padded + 1u, sizeof(oc_real)); /* :136-137 padded_input */
-  memcpy(p, input, dim * sizeof(oc_real));
-  oc_real* corr = corr_out ? corr_out : malloc((padded + 1u) * sizeof(oc_real));
-  oc_real* dec = malloc((chunk + 1u) * sizeof(oc_real));
+  oc_real* p = scratch(S_PAD, (padded + 1u) * sizeof(oc_real)); /* :136-137 padded_input */
+  pcopy(p, input, dim * sizeof(oc_real));
+  for (uint64_t k = dim; k < padded; ++k) p[k] = 0;
+  oc_real* corr = scratch(S_CORR, (chunk + 1u) * sizeof(oc_real)); /* one chunk at a time */
+  double cmax = 0.0;
+  oc_real* dec = scratch(S_DEC, (chunk + 1u) * sizeof(oc_real));
   oc_block b;
-  b.bits = calloc((chunk + 7u) / 8u + 1u, 1);
+  b.bits = scratch(S_WBITS, (chunk + 7u) / 8u + 1u);
   int st = OC_OK;
   for (int j = 0; j < n && st == OC_OK; ++j) {
     const uint64_t off = (uint64_t)j * chunk;
-    st = compress_with_feedback(p + off, werr + off, chunk, kind, es, corr + off, &b);
+    st = compress_with_feedback(p + off, werr + off, chunk, kind, es, corr, &b);
     if (st) break;
+    if (corr_max) {
+      const double mj = max_abs(corr, chunk);
+      cmax = cmax < mj ? mj : cmax;
+    }
     if (kind == 0) block_store(&b, packets + (size_t)j * ipkt_bytes(chunk));
     if (vc && vc->verify && es == 1.0) { /* :145-147 */
       if (kind == 0) block_decompress(b.bits, b.scale, chunk, dec);
-      else memcpy(dec, corr + off, chunk * sizeof(oc_real));
-      st = verify_chunk(vc, corr + off, dec, werr + off, chunk);
+      else memcpy(dec, corr, chunk * sizeof(oc_real));
+      st = verify_chunk(vc, corr, dec, werr + off, chunk);
     }
   }
-  free(b.bits);
-  free(dec);
-  if (!corr_out) free(corr);
-  free(p);
+  if (corr_max) *corr_max = cmax;
   return st;
 }
 
@@ -433,11 +527,16 @@ int oc_worker_compress(const oc_real* stream, uint64_t dim, int n, oc_real* werr
  * scale(1/n) (:164), then compression with the server residual. */
 static int server_avg(const uint8_t* packets, uint64_t chunk, int n, oc_real* avg) {
   const double inv_n = 1.0 / (double)n;
+  const uint64_t n_ = chunk;
+  double sc[64];
+  for (int i = 0; i < n && i < 64; ++i)
+    sc[i] = (double)stored_scale(packets + (size_t)i * ipkt_bytes(chunk), chunk);
+  OC_PAR
   for (uint64_t k = 0; k < chunk; ++k) {
     double acc = 0.0;
     for (int i = 0; i < n; ++i) {
       const uint8_t* pk = packets + (size_t)i * ipkt_bytes(chunk);
-      const double s = (double)stored_scale(pk, chunk);
+      const double s = i < 64 ? sc[i] : (double)stored_scale(pk, chunk);
       if (s == 0.0) continue;
       acc += bit_at(pk, k) ? s : -s;
     }
@@ -448,16 +547,13 @@ static int server_avg(const uint8_t* packets, uint64_t chunk, int n, oc_real* av
 
 int oc_server_reduce(const uint8_t* packets, uint64_t chunk, int n, oc_real* serr, double es,
                      uint8_t* out_packet) {
-  oc_real* avg = malloc((chunk + 1u) * sizeof(oc_real));
-  oc_real* corr = malloc((chunk + 1u) * sizeof(oc_real));
+  oc_real* avg = scratch(S_AVG, (chunk + 1u) * sizeof(oc_real));
+  oc_real* corr = scratch(S_CORR2, (chunk + 1u) * sizeof(oc_real));
   oc_block b;
-  b.bits = calloc((chunk + 7u) / 8u + 1u, 1);
+  b.bits = scratch(S_SBITS, (chunk + 7u) / 8u + 1u);
   server_avg(packets, chunk, n, avg);
   int st = compress_with_feedback(avg, serr, chunk, 0, es, corr, &b);
   if (st == OC_OK) block_store(&b, out_packet);
-  free(b.bits);
-  free(corr);
-  free(avg);
   return st;
 }
 
@@ -470,7 +566,7 @@ static int cluster_compressed(oc_cluster* c, const oc_real* inputs, double es, o
   const int n = c->n;
   const uint64_t P = c->padded, ch = c->chunk, pb = ipkt_bytes(ch);
   int st = OC_OK;
-  oc_real* result = calloc(P + 1u, sizeof(oc_real));
+  oc_real* result = scratch(S_RESULT, (P + 1u) * sizeof(oc_real)); /* every chunk is written */
   if (c->kind == 1) {
     /* Identity compressor: dense messages, residuals stay zero. */
     oc_real* corr_all = malloc(((size_t)n * P + 1u) * sizeof(oc_real));
@@ -482,7 +578,7 @@ static int cluster_compressed(oc_cluster* c, const oc_real* inputs, double es, o
         compress_with_feedback(p + (uint64_t)j * ch, c->werr + (size_t)i * P + (uint64_t)j * ch, ch,
                                1, es, corr_all + (size_t)i * P + (uint64_t)j * ch, &b);
       }
-      memcpy(c->wcorr + (size_t)i * P, corr_all + (size_t)i * P, P * sizeof(oc_real));
+      c->wcmax[i] = max_abs(corr_all + (size_t)i * P, P);
       free(p);
     }
     oc_real* avg = malloc((ch + 1u) * sizeof(oc_real));
@@ -505,17 +601,17 @@ static int cluster_compressed(oc_cluster* c, const oc_real* inputs, double es, o
   } else {
     for (int i = 0; i < n && st == OC_OK; ++i) {
       st = worker_phase(inputs + (size_t)i * c->dim, c->dim, n, 0, c->werr + (size_t)i * P, es,
-                        c->wpk + (size_t)i * (size_t)n * pb, c->wcorr + (size_t)i * P, c);
+                        c->wpk + (size_t)i * (size_t)n * pb, &c->wcmax[i], c);
     }
-    uint8_t* inbox = malloc((size_t)n * pb);
-    oc_real* avg = malloc((ch + 1u) * sizeof(oc_real));
-    oc_real* corr = malloc((ch + 1u) * sizeof(oc_real));
-    oc_real* dec = malloc((ch + 1u) * sizeof(oc_real));
+    uint8_t* inbox = scratch(S_INBOX, (size_t)n * pb);
+    oc_real* avg = scratch(S_AVG, (ch + 1u) * sizeof(oc_real));
+    oc_real* corr = scratch(S_CORR2, (ch + 1u) * sizeof(oc_real));
+    oc_real* dec = scratch(S_DEC2, (ch + 1u) * sizeof(oc_real));
     oc_block b;
-    b.bits = calloc((ch + 7u) / 8u + 1u, 1);
+    b.bits = scratch(S_SBITS, (ch + 7u) / 8u + 1u);
     for (int j = 0; j < n && st == OC_OK; ++j) {
       for (int i = 0; i < n; ++i)
-        memcpy(inbox + (size_t)i * pb, c->wpk + ((size_t)i * (size_t)n + (size_t)j) * pb, pb);
+        pcopy(inbox + (size_t)i * pb, c->wpk + ((size_t)i * (size_t)n + (size_t)j) * pb, pb);
       server_avg(inbox, ch, n, avg);
       oc_real* se = c->serr + (size_t)j * ch;
       st = compress_with_feedback(avg, se, ch, 0, es, corr, &b);
@@ -523,21 +619,15 @@ static int cluster_compressed(oc_cluster* c, const oc_real* inputs, double es, o
       block_store(&b, c->spk + (size_t)j * pb);
       block_decompress(b.bits, b.scale, ch, dec);
       if (c->verify && es == 1.0) st = verify_chunk(c, corr, dec, se, ch);
-      memcpy(result + (uint64_t)j * ch, dec, ch * sizeof(oc_real));
+      pcopy(result + (uint64_t)j * ch, dec, ch * sizeof(oc_real));
       stats_update(&c->sstats[j], sqrt(canonical_sum(se, ch, SUM_SQ)), max_abs(se, ch),
                    max_abs(corr, ch));
     }
-    free(b.bits);
-    free(dec);
-    free(corr);
-    free(avg);
-    free(inbox);
   }
   if (st == OC_OK) {
     for (int i = 0; i < n; ++i) { /* :108-118 refresh_endpoint_stats */
       const oc_real* we = c->werr + (size_t)i * P;
-      stats_update(&c->wstats[i], sqrt(canonical_sum(we, P, SUM_SQ)), max_abs(we, P),
-                   max_abs(c->wcorr + (size_t)i * P, P));
+      stats_update(&c->wstats[i], sqrt(canonical_sum(we, P, SUM_SQ)), max_abs(we, P), c->wcmax[i]);
     }
     uint64_t bits = 0; /* :189-197 ledger */
     for (int j = 0; j < n; ++j) bits += chunk_payload_bits(c, (uint64_t)j);
@@ -546,9 +636,8 @@ static int cluster_compressed(oc_cluster* c, const oc_real* inputs, double es, o
     c->ledger[3] += 2u * (uint64_t)(n - 1) * c->dim * (uint64_t)c->baseline_bits;
     c->ledger[4] += 1;
     if (c->verify && es == 1.0) c->checks += (uint64_t)n * (uint64_t)n + (uint64_t)n;
-    memcpy(out, result, c->dim * sizeof(oc_real)); /* :202 truncate to dim */
+    pcopy(out, result, c->dim * sizeof(oc_real)); /* :202 truncate to dim */
   }
-  free(result);
   return st;
 }
 
@@ -573,6 +662,8 @@ int oc_cluster_compressed_allreduce(void* cv, const oc_real* inputs, double es, 
 int oc_cluster_lossless_allreduce(void* cv, const oc_real* inputs, oc_real* out) {
   oc_cluster* c = cv;
   const double inv_n = 1.0 / (double)c->n;
+  const uint64_t n_ = c->dim;
+  OC_PAR
   for (uint64_t k = 0; k < c->dim; ++k) {
     double acc = 0.0;
     for (int i = 0; i < c->n; ++i) acc += (double)inputs[(size_t)i * c->dim + k];
@@ -588,12 +679,12 @@ int oc_cluster_lossless_allreduce(void* cv, const oc_real* inputs, oc_real* out)
 
 void oc_cluster_worker_error(void* cv, int i, oc_real* out) {
   oc_cluster* c = cv;
-  memcpy(out, c->werr + (size_t)i * c->padded, c->padded * sizeof(oc_real));
+  pcopy(out, c->werr + (size_t)i * c->padded, c->padded * sizeof(oc_real));
 }
 
 void oc_cluster_server_error(void* cv, int j, oc_real* out) {
   oc_cluster* c = cv;
-  memcpy(out, c->serr + (size_t)j * c->chunk, c->chunk * sizeof(oc_real));
+  pcopy(out, c->serr + (size_t)j * c->chunk, c->chunk * sizeof(oc_real));
 }
 
 void oc_cluster_ledger(void* cv, uint64_t* out) { memcpy(out, ((oc_cluster*)cv)->ledger, 48); }
@@ -718,19 +809,27 @@ void oc_opt_free(void* ov) {
 /* Elementwise maps, kernels.cpp:226-305 (each product/sum rounded to real). */
 static void axpby(oc_real* y, double a, double b, const oc_real* x, uint64_t n) {
   const oc_real A = R(a), B = R(b);
+  const uint64_t n_ = n;
+  OC_PAR
   for (uint64_t i = 0; i < n; ++i) y[i] = A * y[i] + B * x[i];
 }
 static void axpby_square(oc_real* y, double a, double b, const oc_real* x, uint64_t n) {
   const oc_real A = R(a), B = R(b);
+  const uint64_t n_ = n;
+  OC_PAR
   for (uint64_t i = 0; i < n; ++i) y[i] = A * y[i] + B * x[i] * x[i];
 }
 static void linear_combine(oc_real* dst, double a, const oc_real* x, double b, const oc_real* y,
                            uint64_t n) {
   const oc_real A = R(a), B = R(b);
+  const uint64_t n_ = n;
+  OC_PAR
   for (uint64_t i = 0; i < n; ++i) dst[i] = A * x[i] + B * y[i];
 }
 static void precondition(oc_real* dst, const oc_real* m, const oc_real* v, double eta, uint64_t n) {
   const oc_real E = R(eta);
+  const uint64_t n_ = n;
+  OC_PAR
   for (uint64_t i = 0; i < n; ++i) {
 #ifdef OC_REAL_FLOAT
     dst[i] = m[i] / (sqrtf(v[i]) + E);
@@ -741,10 +840,14 @@ static void precondition(oc_real* dst, const oc_real* m, const oc_real* v, doubl
 }
 static void axpy(oc_real* y, double a, const oc_real* x, uint64_t n) {
   const oc_real A = R(a);
+  const uint64_t n_ = n;
+  OC_PAR
   for (uint64_t i = 0; i < n; ++i) y[i] += A * x[i];
 }
 static void scale_vec(oc_real* v, double a, uint64_t n) {
   const oc_real A = R(a);
+  const uint64_t n_ = n;
+  OC_PAR
   for (uint64_t i = 0; i < n; ++i) v[i] *= A;
 }
 
@@ -759,7 +862,7 @@ static void lamb_step(oc_opt* o, const oc_real* g, double lr, int track, double*
     oc_real *x = o->x + a, *m = o->m + a, *v = o->v + a;
     axpby(m, h->beta1, 1.0 - h->beta1, g + a, n);
     axpby_square(v, h->beta2, 1.0 - h->beta2, g + a, n);
-    oc_real* u = malloc((n + 1u) * sizeof(oc_real));
+    oc_real* u = scratch(S_U, (n + 1u) * sizeof(oc_real));
     precondition(u, m, v, h->eta, n);
     if (h->wd > 0.0) axpy(u, h->wd, x, n);
     const double xn = sqrt(canonical_sum(x, n, SUM_SQ));
@@ -773,7 +876,6 @@ static void lamb_step(oc_opt* o, const oc_real* g, double lr, int track, double*
     tr[L + l] = 1.0;
     tr[2 * L + l] = sqrt(canonical_sum(v, n, SUM_SQ));
     tr[3 * L + l] = 1.0;
-    free(u);
   }
 }
 
@@ -786,7 +888,7 @@ static void adam_step(oc_opt* o, const oc_real* g, double lr, double* tr) {
     oc_real *x = o->x + a, *m = o->m + a, *v = o->v + a;
     axpby(m, h->beta1, 1.0 - h->beta1, g + a, n);
     axpby_square(v, h->beta2, 1.0 - h->beta2, g + a, n);
-    oc_real* u = malloc((n + 1u) * sizeof(oc_real));
+    oc_real* u = scratch(S_U, (n + 1u) * sizeof(oc_real));
     precondition(u, m, v, h->eta, n);
     if (h->wd > 0.0) axpy(u, h->wd, x, n);
     axpy(x, -lr, u, n);
@@ -794,17 +896,16 @@ static void adam_step(oc_opt* o, const oc_real* g, double lr, double* tr) {
     tr[L + l] = 1.0;
     tr[2 * L + l] = sqrt(canonical_sum(v, n, SUM_SQ));
     tr[3 * L + l] = 1.0;
-    free(u);
   }
 }
 
 /* optimizers.cpp:202-224 finalize_warmup; fusion.cpp:107-125 compute_scales */
 static void finalize_warmup(oc_opt* o) {
   const int L = o->L;
-  memcpy(o->vf, o->v, o->d * sizeof(oc_real));
+  pcopy(o->vf, o->v, o->d * sizeof(oc_real));
   o->has_vf = 1;
   if (o->variant == V_ONEBIT_LAMB) {
-    memcpy(o->mprev, o->m, o->d * sizeof(oc_real));
+    pcopy(o->mprev, o->m, o->d * sizeof(oc_real));
     o->has_mprev = 1;
   }
   if (o->variant == V_ONEBIT_ADAM) {
@@ -842,7 +943,7 @@ static int compressed_step(oc_opt* o, oc_cluster* c, const oc_real* grads, int n
                 "momentum snapshot are missing");
   if (n != c->n)
     return fail(OC_DIMENSION, "compressed step: worker count: size mismatch (%d vs %d)", n, c->n);
-  oc_real* streams = malloc(((size_t)n * d + 1u) * sizeof(oc_real));
+  oc_real* streams = scratch(S_STREAMS, ((size_t)n * d + 1u) * sizeof(oc_real));
   for (int i = 0; i < n; ++i) { /* :248-255 */
     for (int l = 0; l < L; ++l) {
       const uint64_t a = o->off[l], len = o->off[l + 1] - a;
@@ -852,13 +953,9 @@ static int compressed_step(oc_opt* o, oc_cluster* c, const oc_real* grads, int n
     }
   }
   const double es = h->scaled_ef ? o->c_mean_prev2 / o->c_mean_prev : 1.0; /* :226-229 */
-  oc_real* mg = malloc((d + 1u) * sizeof(oc_real));
+  oc_real* mg = scratch(S_MG, (d + 1u) * sizeof(oc_real));
   int st = cluster_compressed(c, streams, es, mg);
-  free(streams);
-  if (st) {
-    free(mg);
-    return st;
-  }
+  if (st) return st;
   for (int l = 0; l < L; ++l) { /* fusion.cpp:139-145 remove_scaling */
     const uint64_t a = o->off[l];
     scale_vec(mg + a, 1.0 / o->coeff[l], o->off[l + 1] - a);
@@ -871,19 +968,15 @@ static int compressed_step(oc_opt* o, oc_cluster* c, const oc_real* grads, int n
     double cc = 1.0, r = 1.0, pre = 1.0;
     if (o->variant == V_ONEBIT_LAMB) {
       if (!o->has_mprev) {
-        free(mg);
         return fail(OC_STAGE_ORDER, "compressed step: momentum snapshot missing");
       }
-      oc_real* rec = malloc((len + 1u) * sizeof(oc_real));
+      oc_real* rec = scratch(S_REC, (len + 1u) * sizeof(oc_real));
       const double inv = 1.0 / (1.0 - h->beta1);
       linear_combine(rec, inv, mgl, -h->beta1 * inv, mp, len); /* :284-287 */
       if (!all_finite(rec, len)) {
-        free(rec);
-        free(mg);
         return fail(OC_RUNTIME, "non-finite reconstructed gradient for layer 'layer%d'", l);
       }
       axpby_square(v, h->beta2, 1.0 - h->beta2, rec, len); /* :294 */
-      free(rec);
       pre = max_abs_ratio(vf, v, len, h->floor_); /* :296 */
       r = clip(pre, (1.0 - h->r_thr) * o->r_prev[l], (1.0 + h->r_thr) * o->r_prev[l]);
       r = clip(r, h->r_min, h->r_max);
@@ -892,26 +985,23 @@ static int compressed_step(oc_opt* o, oc_cluster* c, const oc_real* grads, int n
       cc = o->c_avg[l];
     }
     if (!o->has_vf) {
-      free(mg);
       return fail(OC_STAGE_ORDER, "compressed step: frozen variance missing");
     }
-    oc_real* u = malloc((len + 1u) * sizeof(oc_real));
+    oc_real* u = scratch(S_U, (len + 1u) * sizeof(oc_real));
     precondition(u, mgl, vf, h->eta, len); /* :308-312 */
     if (h->wd > 0.0) axpy(u, h->wd, x, len);
     axpy(x, -lr * cc, u, len); /* :313 */
-    free(u);
     if (o->variant == V_ONEBIT_LAMB) {
-      memcpy(mp, mgl, len * sizeof(oc_real));
+      pcopy(mp, mgl, len * sizeof(oc_real));
       o->r_prev[l] = r;
     }
-    memcpy(m, mgl, len * sizeof(oc_real));
+    pcopy(m, mgl, len * sizeof(oc_real));
     c_sum += cc;
     tr[l] = cc;
     tr[L + l] = r;
     tr[2 * L + l] = sqrt(canonical_sum(v, len, SUM_SQ));
     tr[3 * L + l] = pre;
   }
-  free(mg);
   o->c_mean_prev2 = o->c_mean_prev;
   const double cm = c_sum / (double)L;
   o->c_mean_prev = cm < h->floor_ ? h->floor_ : cm;
@@ -938,11 +1028,10 @@ int oc_opt_step(void* ov, void* cv, const oc_real* grads, int n, uint64_t t, dou
     return fail(OC_DIMENSION, "compressed_allreduce: input length: size mismatch (%llu vs %llu)",
                 (unsigned long long)o->d, (unsigned long long)c->dim);
   if (!is_two_stage(o->variant) || t < o->hp.warmup) {
-    oc_real* avg = malloc((o->d + 1u) * sizeof(oc_real));
+    oc_real* avg = scratch(S_LAVG, (o->d + 1u) * sizeof(oc_real));
     oc_cluster_lossless_allreduce(c, grads, avg); /* :119-138 average_lossless */
     if (o->variant == V_ADAM || o->variant == V_ONEBIT_ADAM) adam_step(o, avg, lr, tr);
     else lamb_step(o, avg, lr, o->variant != V_LAMB, tr);
-    free(avg);
     if (is_two_stage(o->variant) && t + 1u == o->hp.warmup) finalize_warmup(o);
     return OC_OK;
   }
@@ -955,14 +1044,14 @@ void oc_opt_get(void* ov, int which, oc_real* out) {
   oc_opt* o = ov;
   const oc_real* src = which == 0 ? o->x : which == 1 ? o->m : which == 2 ? o->v
                      : which == 3 ? o->vf : o->mprev;
-  memcpy(out, src, o->d * sizeof(oc_real));
+  pcopy(out, src, o->d * sizeof(oc_real));
 }
 
 void oc_opt_set(void* ov, int which, const oc_real* in) {
   oc_opt* o = ov;
   oc_real* dst = which == 0 ? o->x : which == 1 ? o->m : which == 2 ? o->v
                : which == 3 ? o->vf : o->mprev;
-  memcpy(dst, in, o->d * sizeof(oc_real));
+  pcopy(dst, in, o->d * sizeof(oc_real));
   if (which == 3) o->has_vf = 1;
   if (which == 4) o->has_mprev = 1;
 }

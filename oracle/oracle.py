@@ -117,6 +117,8 @@ class Lib:
         if which == "ref":
             so.oc_set_threads.argtypes = [C.c_int]
             so.oc_set_threads.restype = C.c_int
+            so.oc_opt_load_grads.argtypes = [P, P, C.c_int]
+            so.oc_opt_step_loaded.argtypes = [P, P, u64, C.c_double, P, P]
         if which != "ref":
             so.oc_cluster_set_tolerance.argtypes = [P, C.c_double]
             so.oc_cluster_server_packet.argtypes = [P, C.c_int, P]
@@ -287,6 +289,20 @@ class Optimizer:
                                            C.addressof(comp)))
         return {"c": tr[:Ln].copy(), "r": tr[Ln:2 * Ln].copy(), "v_norm": tr[2 * Ln:3 * Ln].copy(),
                 "v_ratio_preclip": tr[3 * Ln:].copy(), "compressed": bool(comp.value)}
+
+    def load_grads(self, grads) -> None:
+        """ref only: convert the n fused gradients once (bench reference arm)."""
+        g = self.L.arr(grads)
+        self.L.check(self.L.so.oc_opt_load_grads(self.h, ptr(g), g.shape[0]))
+
+    def step_loaded(self, t: int, lr: float, cluster: Cluster) -> tuple[float, bool]:
+        """ref only: the stock Optimizer::step on the loaded gradients; returns
+        (seconds measured around the call in C++, compressed)."""
+        sec = C.c_double()
+        comp = C.c_int()
+        self.L.check(self.L.so.oc_opt_step_loaded(self.h, cluster.h, t, lr, C.addressof(sec),
+                                                  C.addressof(comp)))
+        return sec.value, bool(comp.value)
 
     def get(self, name: str) -> np.ndarray:
         out = np.zeros(self.d, dtype=self.L.real)

@@ -15,6 +15,7 @@
 // with the classic test-only `#define private public` before including the
 // headers; the library objects themselves are compiled untouched.
 
+#include <chrono>
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
@@ -88,6 +89,9 @@ int guarded(F&& f) {
 struct OptBox {
   Optimizer opt;
   std::vector<std::size_t> sizes;
+  // bench.py's reference arm: gradients already in the reference's own
+  // [worker][layer] DenseVector form, so only Optimizer::step is timed.
+  std::vector<std::vector<DenseVector>> loaded;
 };
 
 HyperParams unpack_hp(const double* hp, std::uint64_t total, std::uint64_t warmup,
@@ -276,7 +280,7 @@ int oc_opt_new(int variant, const std::uint64_t* sizes, int L, const double* hp,
     }
     auto* box = new OptBox{Optimizer(static_cast<OptimizerVariant>(variant), specs,
                                      unpack_hp(hp, total, warmup, scaled_ef)),
-                           {}};
+                           {}, {}};
     for (int l = 0; l < L; ++l) box->sizes.push_back(sizes[l]);
     *out = box;
   });
@@ -307,6 +311,38 @@ int oc_opt_step(void* o, void* c, const double* grads, int n, std::uint64_t t,
       trace[2 * L + l] = tr.v_norm[l];
       trace[3 * L + l] = tr.v_ratio_preclip[l];
     }
+    *compressed = tr.compressed ? 1 : 0;
+  });
+}
+
+// Bench support (bench.py --impl reference): convert n fused gradients once
+// into the caller-side form Optimizer::step takes (optimizers.hpp:106-107),
+// then time the stock step alone with steady_clock.
+int oc_opt_load_grads(void* o, const double* grads, int n) {
+  auto* box = static_cast<OptBox*>(o);
+  return guarded([&] {
+    const std::size_t d = box->opt.fused_dim();
+    box->loaded.assign(static_cast<std::size_t>(n), {});
+    for (int i = 0; i < n; ++i) {
+      std::size_t off = 0;
+      for (std::size_t sz : box->sizes) {
+        box->loaded[static_cast<std::size_t>(i)].emplace_back(
+            std::span<const double>(grads + static_cast<std::size_t>(i) * d + off, sz));
+        off += sz;
+      }
+    }
+  });
+}
+
+int oc_opt_step_loaded(void* o, void* c, std::uint64_t t, double lr, double* seconds,
+                       int* compressed) {
+  auto* box = static_cast<OptBox*>(o);
+  auto* cl = static_cast<SimCluster*>(c);
+  return guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    StepTrace tr = box->opt.step(box->loaded, t, lr, *cl);
+    const auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
     *compressed = tr.compressed ? 1 : 0;
   });
 }

@@ -9,8 +9,10 @@ without the library fails, and creating a cluster without a GPU raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
+import sys
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -119,6 +121,8 @@ def _load() -> C.CDLL:
     so.bl_cluster_dims.argtypes = [P, C.POINTER(u64), C.POINTER(u64)]
     so.bl_cluster_transport.argtypes = [P]
     so.bl_cluster_transport.restype = i32
+    so.bl_cluster_stream.argtypes = [P]
+    so.bl_cluster_stream.restype = P
     so.bl_cluster_compressed_allreduce.argtypes = [P, P, i32, u64, P, C.c_double, i32]
     so.bl_cluster_lossless_allreduce.argtypes = [P, P, i32, u64, P, i32]
     so.bl_cluster_worker_error.argtypes = [P, i32, P]
@@ -253,6 +257,22 @@ def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
 
+def _torch_cuda_live() -> bool:
+    """True once this process has touched CUDA through torch (its current
+    stream may then hold pending writes into buffers the library reads)."""
+    t = sys.modules.get("torch")
+    return bool(t is not None and t.cuda.is_initialized())
+
+
+class _DeviceView:
+    """__cuda_array_interface__ over a library-owned device buffer, so torch
+    can alias it without a copy (torch.as_tensor)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
 def _pointers(inputs, length: int):
     """-> (ctypes array of pointers, memory kind, keepalive list)."""
     if _is_torch_cuda(inputs):
@@ -320,6 +340,36 @@ class SimCluster:
         p, c = C.c_uint64(), C.c_uint64()
         _check(_lib.bl_cluster_dims(self._h, C.byref(p), C.byref(c)))
         self.padded, self.chunk_len = p.value, c.value
+        self._stream_ptr = int(_lib.bl_cluster_stream(self._h) or 0)
+        self._ext = None
+
+    @contextlib.contextmanager
+    def torch_ordered(self, tensors=()):
+        """Order the library's stream after torch's current stream on entry
+        (inputs written by torch kernels) and torch's after the library's on
+        exit (outputs read by torch kernels); torch temporaries handed to the
+        library are recorded on its stream so the caching allocator does not
+        reuse them while an asynchronous copy may still read them."""
+        if not tensors and not _torch_cuda_live():
+            yield
+            return
+        import torch
+
+        dev = torch.device("cuda", self.device)
+        if self._ext is None:
+            self._ext = torch.cuda.ExternalStream(self._stream_ptr, device=dev)
+        cur = torch.cuda.current_stream(dev)
+        same = cur.cuda_stream == self._stream_ptr
+        if not same:
+            self._ext.wait_stream(cur)
+        try:
+            yield
+        finally:
+            if not same:
+                cur.wait_stream(self._ext)
+                for t in tensors:
+                    if _is_torch_cuda(t):
+                        t.record_stream(self._ext)
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -362,8 +412,9 @@ class SimCluster:
 
             if out is None:
                 out = torch.empty(self._dim, dtype=torch.float32, device=f"cuda:{self.device}")
-            _check(_lib.bl_cluster_compressed_allreduce(self._h, ptrs, n_in, length, out.data_ptr(),
-                                                        error_scale, mem))
+            with self.torch_ordered(keep + [out]):
+                _check(_lib.bl_cluster_compressed_allreduce(self._h, ptrs, n_in, length, out.data_ptr(),
+                                                            error_scale, mem))
             return out
         res = np.zeros(max(self._dim, 1), dtype=np.float32)
         _check(_lib.bl_cluster_compressed_allreduce(self._h, ptrs, n_in, length, res.ctypes.data,
@@ -375,9 +426,17 @@ class SimCluster:
         buffers (zero-copy); `out` is a torch CUDA tensor of dim floats."""
         nw = self.local_workers()
         ptrs = (C.c_void_p * nw)(*[self.input_buffer(i) for i in range(nw)])
-        _check(_lib.bl_cluster_compressed_allreduce(self._h, ptrs, nw, self._dim, out.data_ptr(),
-                                                    error_scale, MEM_DEVICE))
+        with self.torch_ordered([out]):
+            _check(_lib.bl_cluster_compressed_allreduce(self._h, ptrs, nw, self._dim, out.data_ptr(),
+                                                        error_scale, MEM_DEVICE))
         return out
+
+    def input_tensor(self, worker: int):
+        """torch view (no copy) of worker's dim-float input buffer."""
+        import torch
+
+        return torch.as_tensor(_DeviceView(self.input_buffer(worker), self._dim),
+                               device=f"cuda:{self.device}")
 
     def lossless_allreduce(self, inputs):
         """comm_sim.hpp:102."""
@@ -386,7 +445,9 @@ class SimCluster:
             import torch
 
             out = torch.empty(self._dim, dtype=torch.float32, device=f"cuda:{self.device}")
-            _check(_lib.bl_cluster_lossless_allreduce(self._h, ptrs, n_in, length, out.data_ptr(), mem))
+            with self.torch_ordered(keep + [out]):
+                _check(_lib.bl_cluster_lossless_allreduce(self._h, ptrs, n_in, length, out.data_ptr(),
+                                                          mem))
             return out
         res = np.zeros(self._dim, dtype=np.float32)
         _check(_lib.bl_cluster_lossless_allreduce(self._h, ptrs, n_in, length, res.ctypes.data, mem))
@@ -498,6 +559,14 @@ class Optimizer:
     def grad_buffer(self, worker: int) -> int:
         return int(_lib.bl_optimizer_grad_buffer(self._h, worker))
 
+    def grad_tensor(self, worker: int):
+        """torch view (no copy) of worker's device gradient buffer: write the
+        gradient into it, then step_resident()."""
+        import torch
+
+        return torch.as_tensor(_DeviceView(self.grad_buffer(worker), self.fused_dim()),
+                               device=f"cuda:{self.cluster.device}")
+
     def _fuse(self, local_grads):
         """[worker][layer] arrays, [worker] fused arrays, or a 2-D array."""
         if isinstance(local_grads, np.ndarray) or _is_torch_cuda(local_grads):
@@ -519,11 +588,13 @@ class Optimizer:
             raise DimensionError(f"step: gradient length: size mismatch ({length} vs {self.fused_dim()})")
         L = len(self.sizes)
         if not trace:
-            _check(_lib.bl_optimizer_step(self._h, cluster.handle, ptrs, n_in, t, lr, mem, None))
+            with cluster.torch_ordered(keep if mem == MEM_DEVICE else ()):
+                _check(_lib.bl_optimizer_step(self._h, cluster.handle, ptrs, n_in, t, lr, mem, None))
             return None
         arrs = [np.zeros(L, dtype=np.float64) for _ in range(4)]
         tr = _Trace(*[a.ctypes.data for a in arrs], 0)
-        _check(_lib.bl_optimizer_step(self._h, cluster.handle, ptrs, n_in, t, lr, mem, C.byref(tr)))
+        with cluster.torch_ordered(keep if mem == MEM_DEVICE else ()):
+            _check(_lib.bl_optimizer_step(self._h, cluster.handle, ptrs, n_in, t, lr, mem, C.byref(tr)))
         return StepTrace(arrs[0], arrs[1], arrs[2], arrs[3], bool(tr.compressed))
 
     def step_resident(self, t: int, lr: float, trace: bool = False) -> StepTrace | None:
@@ -541,11 +612,13 @@ class Optimizer:
     def _step_ptrs(self, ptrs, n, t, lr, mem, trace):
         L = len(self.sizes)
         if not trace:
-            _check(_lib.bl_optimizer_step(self._h, self.cluster.handle, ptrs, n, t, lr, mem, None))
+            with self.cluster.torch_ordered():
+                _check(_lib.bl_optimizer_step(self._h, self.cluster.handle, ptrs, n, t, lr, mem, None))
             return None
         arrs = [np.zeros(L, dtype=np.float64) for _ in range(4)]
         tr = _Trace(*[a.ctypes.data for a in arrs], 0)
-        _check(_lib.bl_optimizer_step(self._h, self.cluster.handle, ptrs, n, t, lr, mem, C.byref(tr)))
+        with self.cluster.torch_ordered():
+            _check(_lib.bl_optimizer_step(self._h, self.cluster.handle, ptrs, n, t, lr, mem, C.byref(tr)))
         return StepTrace(arrs[0], arrs[1], arrs[2], arrs[3], bool(tr.compressed))
 
     def get(self, name: str) -> np.ndarray:

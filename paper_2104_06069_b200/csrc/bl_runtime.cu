@@ -1138,6 +1138,7 @@ void bl_cluster_destroy(bl_cluster* c) {
 }
 
 int32_t bl_cluster_transport(const bl_cluster* c) { return c ? c->transport : BL_TRANSPORT_NCCL; }
+void* bl_cluster_stream(const bl_cluster* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
 bl_status bl_cluster_dims(const bl_cluster* c, uint64_t* padded, uint64_t* chunk) {
   return guarded([&] {
