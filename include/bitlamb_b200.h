@@ -14,6 +14,16 @@
  * returns host data (trace, getters) synchronizes that stream; otherwise
  * calls are asynchronous and device-side failures (non-finite inputs) are
  * reported by the next synchronizing call.
+ *
+ * Transactional steps.  Every step / collective starts with a device-side
+ * gate.  In strict mode (bl_optimizer_set_strict) a read-only pre-pass checks
+ * every gradient first, as Optimizer::check_gradients does before touching any
+ * state (optimizers.cpp:99-117,337); multi-process, the gate is also the
+ * step's arrival barrier.  A failure there (non-finite gradient on any rank, a
+ * rank late past the peer timeout) aborts the step on every rank before any
+ * state changes: the next synchronizing call raises it and the object stays
+ * usable with its state as before the step.  A peer that dies INSIDE a step is
+ * fail-stop: the error is raised and the cluster refuses further work.
  */
 #ifndef BITLAMB_B200_H_
 #define BITLAMB_B200_H_
@@ -25,7 +35,7 @@
 extern "C" {
 #endif
 
-#define BL_ABI_VERSION 1
+#define BL_ABI_VERSION 2
 #define BL_NCCL_UNIQUE_ID_BYTES 128
 
 /* Status codes: errors.hpp:26-53 + check_arg / runtime_error uses. */
@@ -133,6 +143,12 @@ typedef struct bl_step_trace {
   int32_t compressed;
 } bl_step_trace;
 
+/* Optimizer::LayerSpec, optimizers.hpp:95-98. */
+typedef struct bl_layer_spec {
+  const char* name;
+  uint64_t size;
+} bl_layer_spec;
+
 typedef struct bl_cluster bl_cluster;
 typedef struct bl_optimizer bl_optimizer;
 
@@ -156,6 +172,16 @@ int32_t bl_cluster_transport(const bl_cluster* c);
  * optimizer is enqueued on.  Callers that produce inputs on another stream
  * make this stream wait on theirs (and theirs on this one for outputs). */
 void* bl_cluster_stream(const bl_cluster* c);
+/* SimCluster::config() (comm_sim.hpp:105): the configuration the cluster was
+ * created with (transport resolved). */
+bl_status bl_cluster_get_config(const bl_cluster* c, bl_cluster_config* out);
+/* SimCluster::step_count() (comm_sim.hpp:108; incremented per compressed and
+ * per lossless collective, comm_sim.cpp:197,230). */
+uint64_t bl_cluster_step_count(const bl_cluster* c);
+/* Bound of every wait on a peer (multi-process), default 600000 ms.  A rank
+ * that does not arrive at a step within it aborts that step on every rank
+ * (state unchanged); a peer silent inside a step fails the cluster. */
+bl_status bl_cluster_set_peer_timeout(bl_cluster* c, double ms);
 
 /* SimCluster::compressed_allreduce (comm_sim.hpp:98-99, comm_sim.cpp:120-203).
  * inputs[i] is worker i's stream of `len` floats (len must equal dim,
@@ -212,6 +238,17 @@ bl_status bl_volume_reduction(double warmup_ratio, double baseline_bits,
  * optimizer lives on the cluster's device and stream. */
 bl_status bl_optimizer_create(int32_t variant, const uint64_t* layer_sizes, int32_t n_layers,
                               const bl_hparams* hp, bl_cluster* cluster, bl_optimizer** out);
+/* The same with Optimizer::LayerSpec {name, size} (optimizers.hpp:95-101):
+ * the names appear in error messages exactly as the reference prints them. */
+bl_status bl_optimizer_create_named(int32_t variant, const bl_layer_spec* layers, int32_t n_layers,
+                                    const bl_hparams* hp, bl_cluster* cluster, bl_optimizer** out);
+const char* bl_optimizer_layer_name(const bl_optimizer* o, int32_t layer);
+/* Strict mode: check_gradients (optimizers.cpp:99-117) as a read-only
+ * pre-pass before any state changes (+4 bytes/param read per step; with
+ * multi-process every rank raises the same error).  Default off: the finite
+ * check is fused into the first kernel that reads the gradient and reported
+ * by the next synchronizing call, after the step was applied. */
+bl_status bl_optimizer_set_strict(bl_optimizer* o, int32_t on);
 void bl_optimizer_destroy(bl_optimizer* o);
 
 /* Optimizer::step (optimizers.hpp:106-107, optimizers.cpp:334-364).
@@ -235,6 +272,32 @@ bl_status bl_optimizer_set_scalars(bl_optimizer* o, const double* c_avg, const d
 int32_t bl_optimizer_frozen(const bl_optimizer* o);     /* frozen() */
 uint64_t bl_optimizer_fused_dim(const bl_optimizer* o); /* fused_dim() */
 int32_t bl_optimizer_layer_count(const bl_optimizer* o);
+
+/* ---- Free functions (compression.hpp:106-118, fusion.hpp:92-102) -------- */
+
+/* compress_with_feedback (compression.hpp:111-118, compression.cpp:166-198) on
+ * the device: corrected = v + error_scale * delta is compressed (sign bits +
+ * scale mean|corrected|, or the identity message), and delta is replaced by
+ * v + delta - decompress(message) (identity: 0).  wire_out (host, may be NULL):
+ * serialize() bytes, ceil(len/8) sign bytes + LE fp32 scale (one-bit only);
+ * decompressed_out (may be NULL): the len decompressed floats.  v, delta and
+ * decompressed_out live in `memory`.  Non-finite scale: BL_ERR_INVALID_ARGUMENT. */
+bl_status bl_compress_with_feedback(const float* v, float* delta, uint64_t len, int32_t compressor,
+                                    double error_scale, uint8_t* wire_out, float* decompressed_out,
+                                    int32_t memory, int32_t device);
+/* compute_scales (fusion.hpp:92-93, fusion.cpp:107-125): s_l = max(mean|m_l|,
+ * floor), reference = mean_l s_l, coeff_l = reference / s_l over the fused
+ * (layer-major) momentum m of sum(layer_sizes) floats in `memory`.  coeff_out
+ * (n_layers doubles) and reference_out are host memory. */
+bl_status bl_compute_scales(const float* m, const uint64_t* layer_sizes, int32_t n_layers,
+                            double floor, double* coeff_out, double* reference_out, int32_t memory,
+                            int32_t device);
+/* apply_scaling / remove_scaling (fusion.hpp:96-102, fusion.cpp:127-149): each
+ * layer segment of the fused buffer is multiplied by coeff_l / by 1/coeff_l. */
+bl_status bl_apply_scaling(float* fused, const uint64_t* layer_sizes, int32_t n_layers,
+                           const double* coeff, int32_t memory, int32_t device);
+bl_status bl_remove_scaling(float* fused, const uint64_t* layer_sizes, int32_t n_layers,
+                            const double* coeff, int32_t memory, int32_t device);
 
 #ifdef __cplusplus
 }

@@ -209,6 +209,16 @@ class SimCluster {
   double run_max_corrected_linf() const { return max_of(&EndpointStats::max_corrected_linf); }
   std::uint64_t compensation_checks() const { return bl_cluster_compensation_checks(h_); }
 
+  // comm_sim.hpp:105,108
+  bl_cluster_config config() const {
+    bl_cluster_config c{};
+    check(bl_cluster_get_config(h_, &c));
+    return c;
+  }
+  std::size_t step_count() const { return bl_cluster_step_count(h_); }
+  // Bound of every wait on a peer (multi-process); see bitlamb_b200.h.
+  void set_peer_timeout_ms(double ms) { check(bl_cluster_set_peer_timeout(h_, ms)); }
+
   int n_workers() const { return n_; }
   std::size_t dim() const { return dim_; }
   std::size_t padded() const { return padded_; }
@@ -258,15 +268,15 @@ class Optimizer {
   Optimizer(OptimizerVariant variant, std::span<const LayerSpec> layout, const HyperParams& hp,
             SimCluster& cluster)
       : cluster_(&cluster) {
-    std::vector<std::uint64_t> sizes;
-    for (const auto& s : layout) {
-      sizes.push_back(s.size);
-      names_.push_back(s.name);
-    }
+    std::vector<bl_layer_spec> specs;
+    for (const auto& s : layout) names_.push_back(s.name);
+    for (std::size_t l = 0; l < layout.size(); ++l) specs.push_back({names_[l].c_str(), layout[l].size});
     const bl_hparams h = hp.to_c();
-    check(bl_optimizer_create(static_cast<int32_t>(variant), sizes.data(),
-                              static_cast<int32_t>(sizes.size()), &h, cluster.handle(), &h_));
+    check(bl_optimizer_create_named(static_cast<int32_t>(variant), specs.data(),
+                                    static_cast<int32_t>(specs.size()), &h, cluster.handle(), &h_));
   }
+  // Strict mode: check_gradients before any state changes (bitlamb_b200.h).
+  void set_strict(bool on) { check(bl_optimizer_set_strict(h_, on ? 1 : 0)); }
   ~Optimizer() { bl_optimizer_destroy(h_); }
   Optimizer(const Optimizer&) = delete;
   Optimizer& operator=(const Optimizer&) = delete;
@@ -310,6 +320,51 @@ class Optimizer {
   bl_optimizer* h_ = nullptr;
   std::vector<std::string> names_;
 };
+
+// ---- free functions (compression.hpp:106-118, fusion.hpp:92-102) -----------
+struct CompressResult {
+  std::vector<std::uint8_t> wire;  // serialize() bytes (one-bit)
+  std::vector<float> decompressed;
+};
+
+// compress_with_feedback: delta is updated in place.
+inline CompressResult compress_with_feedback(std::span<const float> v, std::span<float> delta,
+                                             CompressorKind kind, double error_scale = 1.0,
+                                             int device = 0) {
+  if (v.size() != delta.size()) throw DimensionError("compress_with_feedback: size mismatch");
+  CompressResult r;
+  r.wire.resize((v.size() + 7) / 8 + 4);
+  r.decompressed.resize(v.size());
+  check(bl_compress_with_feedback(v.data(), delta.data(), v.size(), static_cast<int32_t>(kind), error_scale,
+                                  r.wire.data(), r.decompressed.data(), BL_MEM_HOST, device));
+  return r;
+}
+
+struct MomentumScales {  // fusion.hpp:80-89
+  std::vector<double> coeff;
+  double reference_scale = 1.0;
+};
+
+inline MomentumScales compute_scales(std::span<const float> fused_m, std::span<const std::uint64_t> sizes,
+                                     double floor = 1e-12, int device = 0) {
+  MomentumScales s;
+  s.coeff.resize(sizes.size());
+  check(bl_compute_scales(fused_m.data(), sizes.data(), static_cast<int32_t>(sizes.size()), floor,
+                          s.coeff.data(), &s.reference_scale, BL_MEM_HOST, device));
+  return s;
+}
+inline void apply_scaling(std::span<float> fused, std::span<const std::uint64_t> sizes,
+                          const MomentumScales& s, int device = 0) {
+  if (s.coeff.size() != sizes.size()) throw DimensionError("apply_scaling: size mismatch");
+  check(bl_apply_scaling(fused.data(), sizes.data(), static_cast<int32_t>(sizes.size()), s.coeff.data(),
+                         BL_MEM_HOST, device));
+}
+inline void remove_scaling(std::span<float> fused, std::span<const std::uint64_t> sizes,
+                           const MomentumScales& s, int device = 0) {
+  if (s.coeff.size() != sizes.size()) throw DimensionError("remove_scaling: size mismatch");
+  check(bl_remove_scaling(fused.data(), sizes.data(), static_cast<int32_t>(sizes.size()), s.coeff.data(),
+                          BL_MEM_HOST, device));
+}
 
 }  // namespace bitlamb_b200
 

@@ -102,6 +102,10 @@ class _HParams(C.Structure):
                 ("scaled_error_feedback", C.c_int32)]
 
 
+class _LayerSpec(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("size", C.c_uint64)]
+
+
 class _Trace(C.Structure):
     _fields_ = [("c", C.c_void_p), ("r", C.c_void_p), ("v_norm", C.c_void_p),
                 ("v_ratio_preclip", C.c_void_p), ("compressed", C.c_int32)]
@@ -123,6 +127,18 @@ def _load() -> C.CDLL:
     so.bl_cluster_transport.restype = i32
     so.bl_cluster_stream.argtypes = [P]
     so.bl_cluster_stream.restype = P
+    so.bl_cluster_get_config.argtypes = [P, C.POINTER(_ClusterConfig)]
+    so.bl_cluster_step_count.argtypes = [P]
+    so.bl_cluster_step_count.restype = u64
+    so.bl_cluster_set_peer_timeout.argtypes = [P, C.c_double]
+    so.bl_optimizer_create_named.argtypes = [i32, P, i32, C.POINTER(_HParams), P, C.POINTER(P)]
+    so.bl_optimizer_layer_name.argtypes = [P, i32]
+    so.bl_optimizer_layer_name.restype = C.c_char_p
+    so.bl_optimizer_set_strict.argtypes = [P, i32]
+    so.bl_compress_with_feedback.argtypes = [P, P, u64, i32, C.c_double, P, P, i32, i32]
+    so.bl_compute_scales.argtypes = [P, P, i32, C.c_double, P, P, i32, i32]
+    so.bl_apply_scaling.argtypes = [P, P, i32, P, i32, i32]
+    so.bl_remove_scaling.argtypes = [P, P, i32, P, i32, i32]
     so.bl_cluster_compressed_allreduce.argtypes = [P, P, i32, u64, P, C.c_double, i32]
     so.bl_cluster_lossless_allreduce.argtypes = [P, P, i32, u64, P, i32]
     so.bl_cluster_worker_error.argtypes = [P, i32, P]
@@ -184,6 +200,59 @@ def volume_reduction(warmup_ratio: float, baseline_bits: float,
     _check(_lib.bl_volume_reduction(warmup_ratio, baseline_bits, compressed_bits_per_element,
                                     C.byref(out)))
     return out.value
+
+
+def compress_with_feedback(v, delta, kind: str = "onebit", error_scale: float = 1.0, device: int = 0):
+    """compression.hpp:106-118 on the device.  `delta` (float32 numpy) is
+    updated in place; returns (serialize() bytes or None, decompressed)."""
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    if not (isinstance(delta, np.ndarray) and delta.dtype == np.float32 and delta.flags.c_contiguous):
+        raise InvalidArgument("compress_with_feedback: delta must be a contiguous float32 array")
+    if v.shape != delta.shape:
+        raise DimensionError(f"compress_with_feedback: size mismatch ({v.size} vs {delta.size})")
+    n = v.size
+    wire = np.zeros((n + 7) // 8 + 4, dtype=np.uint8)
+    dec = np.zeros(max(n, 1), dtype=np.float32)
+    _check(_lib.bl_compress_with_feedback(v.ctypes.data, delta.ctypes.data, n, COMPRESSORS[kind],
+                                          error_scale, wire.ctypes.data, dec.ctypes.data, MEM_HOST, device))
+    return (wire.tobytes() if kind == "onebit" else None), dec[:n]
+
+
+def _sizes(sizes) -> np.ndarray:
+    return np.ascontiguousarray([int(x) for x in sizes], dtype=np.uint64)
+
+
+def compute_scales(fused_m, sizes, floor: float = 1e-12, device: int = 0):
+    """fusion.hpp:92-93: -> (coeff[L], reference_scale)."""
+    m = np.ascontiguousarray(fused_m, dtype=np.float32)
+    sz = _sizes(sizes)
+    coeff = np.zeros(max(len(sz), 1), dtype=np.float64)
+    ref = C.c_double()
+    _check(_lib.bl_compute_scales(m.ctypes.data, sz.ctypes.data, len(sz), floor, coeff.ctypes.data,
+                                  C.byref(ref), MEM_HOST, device))
+    return coeff[: len(sz)], ref.value
+
+
+def apply_scaling(fused, sizes, coeff, device: int = 0) -> np.ndarray:
+    """fusion.hpp:96-98: returns fused * coeff per layer."""
+    x = np.array(fused, dtype=np.float32, copy=True)
+    sz = _sizes(sizes)
+    co = np.ascontiguousarray(coeff, dtype=np.float64)
+    if co.size != sz.size:
+        raise DimensionError("apply_scaling: size mismatch")
+    _check(_lib.bl_apply_scaling(x.ctypes.data, sz.ctypes.data, len(sz), co.ctypes.data, MEM_HOST, device))
+    return x
+
+
+def remove_scaling(fused, sizes, coeff, device: int = 0) -> np.ndarray:
+    """fusion.hpp:100-102: returns fused * (1/coeff) per layer."""
+    x = np.array(fused, dtype=np.float32, copy=True)
+    sz = _sizes(sizes)
+    co = np.ascontiguousarray(coeff, dtype=np.float64)
+    if co.size != sz.size:
+        raise DimensionError("remove_scaling: size mismatch")
+    _check(_lib.bl_remove_scaling(x.ctypes.data, sz.ctypes.data, len(sz), co.ctypes.data, MEM_HOST, device))
+    return x
 
 
 @dataclass
@@ -393,6 +462,24 @@ class SimCluster:
     def n_workers(self) -> int:
         return self._n
 
+    def config(self) -> dict:
+        """comm_sim.hpp:105."""
+        c = _ClusterConfig()
+        _check(_lib.bl_cluster_get_config(self._h, C.byref(c)))
+        return {"n_workers": c.n_workers, "dim": c.dim,
+                "compressor": {v: k for k, v in COMPRESSORS.items()}[c.compressor],
+                "baseline_bits_per_element": c.baseline_bits_per_element,
+                "verify_compensation": bool(c.verify_compensation),
+                "compensation_tolerance": c.compensation_tolerance,
+                "endpoint_stats": bool(c.endpoint_stats)}
+
+    def step_count(self) -> int:
+        """comm_sim.hpp:108 (compressed + lossless collectives)."""
+        return int(_lib.bl_cluster_step_count(self._h))
+
+    def set_peer_timeout(self, ms: float) -> None:
+        _check(_lib.bl_cluster_set_peer_timeout(self._h, float(ms)))
+
     def dim(self) -> int:
         return self._dim
 
@@ -527,19 +614,25 @@ class SimCluster:
 class Optimizer:
     """bitlamb::Optimizer (optimizers.hpp:93-145) on B200; state stays in HBM."""
 
-    def __init__(self, variant: str, layout, hp: HyperParams, cluster: SimCluster):
+    def __init__(self, variant: str, layout, hp: HyperParams, cluster: SimCluster, strict: bool = False):
         self.sizes = [int(s[1]) if isinstance(s, (tuple, list)) else int(s) for s in layout]
         self.names = [s[0] if isinstance(s, (tuple, list)) else f"layer{i}"
                       for i, s in enumerate(layout)]
         self.variant = variant
         self.hp = hp
         self.cluster = cluster
-        sz = np.asarray(self.sizes, dtype=np.uint64)
+        self._names_b = [n.encode() for n in self.names]
+        specs = (_LayerSpec * max(1, len(self.sizes)))()
+        for i, (nm, sz) in enumerate(zip(self._names_b, self.sizes)):
+            specs[i].name = nm
+            specs[i].size = sz
         h = C.c_void_p()
         hpc = hp._c()
-        _check(_lib.bl_optimizer_create(VARIANTS[variant], sz.ctypes.data, len(self.sizes),
-                                        C.byref(hpc), cluster.handle, C.byref(h)))
+        _check(_lib.bl_optimizer_create_named(VARIANTS[variant], specs, len(self.sizes),
+                                              C.byref(hpc), cluster.handle, C.byref(h)))
         self._h = h
+        if strict:
+            self.set_strict(True)
         self.offsets = np.concatenate([[0], np.cumsum(self.sizes)]).astype(np.int64)
 
     def close(self) -> None:
@@ -552,6 +645,16 @@ class Optimizer:
 
     def fused_dim(self) -> int:
         return int(_lib.bl_optimizer_fused_dim(self._h))
+
+    def set_strict(self, on: bool) -> None:
+        """check_gradients (optimizers.cpp:99-117) before any state changes."""
+        _check(_lib.bl_optimizer_set_strict(self._h, int(bool(on))))
+
+    def layer_name(self, l: int) -> str:
+        r = _lib.bl_optimizer_layer_name(self._h, l)
+        if r is None:
+            raise InvalidArgument("layer index out of range")
+        return r.decode()
 
     def frozen(self) -> bool:
         return bool(_lib.bl_optimizer_frozen(self._h))

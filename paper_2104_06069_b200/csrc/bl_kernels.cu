@@ -296,6 +296,31 @@ __device__ __forceinline__ void flag(unsigned long long* err, int slot, unsigned
   if (err) atomicMin(err + slot, key);
 }
 
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+// The step gate (bl_kernels.cuh GateReason).  Closed -> every mutating kernel
+// of the cluster returns at entry, leaving the state as it was.
+__device__ __forceinline__ bool gate_closed(const unsigned long long* err) {
+  return err != nullptr && ld_volatile_u64(err + kErrGate) != ~0ull;
+}
+// Kernel-entry form: out of line, so the check leaves the register
+// allocation of the streaming loops that follow untouched (measured: an
+// inlined early return cost K5 extra spills and 10% of its time).
+__device__ __noinline__ bool gate_closed_call(const unsigned long long* err) { return gate_closed(err); }
+__device__ __forceinline__ void close_gate(unsigned long long* err, unsigned long long reason) {
+  if (err) atomicMin(err + kErrGate, reason);
+}
+__device__ __forceinline__ unsigned long long now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Peer wait bound (ns), set by the host in the configuration word.
+__device__ __forceinline__ unsigned long long wait_bound(const unsigned long long* err) {
+  return err ? ld_volatile_u64(err + kCfgTimeout) : (60ull * 1000000000ull);
+}
+
 // Tile scheduler.  With a counter, warps take the next tile from it
 // (dynamic: the slowest warp finishes at most one tile after the others
 // instead of a whole grid-stride share); without, the fixed grid-stride
@@ -336,23 +361,29 @@ __device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned l
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Thread 0 of the block waits until flags[0..n) >= epoch (bounded: a peer that
-// never signals sets kErrPeer instead of hanging the GPU), then the block syncs.
-__device__ __forceinline__ void wait_peers(const unsigned long long* flags, int n,
+// Thread 0 of the block waits until flags[0..n) >= epoch, then the block
+// syncs.  Fail-stop: a peer silent for longer than the configured bound
+// (peer_timeout_ms) sets kErrPeer and closes the gate (kGateMidStep), so
+// nothing later consumes the stale slots; the host then reports the cluster
+// as failed.  Returns false when the gate is closed.
+__device__ __forceinline__ bool wait_peers(const unsigned long long* flags, int n,
                                            unsigned long long epoch, unsigned long long* err) {
   if (threadIdx.x == 0) {
-    for (int i = 0; i < n; ++i) {
-      long long spins = 0;
+    const unsigned long long bound = wait_bound(err), t0 = now_ns();
+    for (int i = 0; i < n && !gate_closed(err); ++i) {
       while (ld_acquire_sys(flags + i) < epoch) {
-        __nanosleep(128);
-        if (++spins > (1ll << 25)) {  // ~5 s
+        if (gate_closed(err)) break;  // another block already timed out
+        __nanosleep(64);
+        if (now_ns() - t0 > bound) {
           flag(err, kErrPeer, static_cast<unsigned long long>(i));
+          close_gate(err, kGateMidStep);
           break;
         }
       }
     }
   }
   __syncthreads();
+  return !gate_closed(err);
 }
 
 // ---------------------------------------------------------------------------
@@ -378,6 +409,21 @@ __device__ __forceinline__ void wait_peers(const unsigned long long* flags, int 
 #ifndef K1_MINB
 #define K1_MINB 2  // resident CTAs per SM requested from ptxas
 #endif
+// check_gradients' finding (optimizers.cpp:99-117) in fused mode, local
+// error word; multi-process it is forwarded to every peer by the kernel that
+// raises this rank's flags (finalize / lossless), so every rank raises.
+__device__ __forceinline__ void flag_grad(const K1Params& p, unsigned long long key) {
+  flag(p.err, kErrGrad, key);
+}
+// Forward this rank's kErrGrad finding to every peer (before its flags rise).
+__device__ __forceinline__ void forward_grad_error(const unsigned long long* err,
+                                                   unsigned long long* const* peer_err, int n) {
+  if (!peer_err || !err) return;
+  const unsigned long long key = ld_volatile_u64(err + kErrGrad);
+  if (key == ~0ull) return;
+  for (int q = 0; q < n; ++q) atomicMin_system(peer_err[q] + kErrGrad, key);
+}
+
 template <int MODE, bool ALIGNED>
 __device__ __forceinline__ void k1_tile(const K1Params& p, long long tile, int lane, uint32_t* sw,
                                         float es) {
@@ -454,9 +500,8 @@ __device__ __forceinline__ void k1_tile(const K1Params& p, long long tile, int l
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             if (!isfinite(comp(g[k], q))) {
-              flag(p.err, kErrGrad,
-                   (static_cast<unsigned long long>(p.worker_base + w) << 40) |
-                       (kc + i0 + (r0 + k) * kRowElems + 4 * lane + q));
+              flag_grad(p, (static_cast<unsigned long long>(p.worker_base + w) << 40) |
+                               (kc + i0 + (r0 + k) * kRowElems + 4 * lane + q));
             }
           }
         }
@@ -559,8 +604,7 @@ __device__ __forceinline__ void k1_tile(const K1Params& p, long long tile, int l
       for (int q = 0; q < 4; ++q) {
         const uint64_t k = kr + 4 * lane + q;
         if (ir + 4 * lane + q < p.c && k < p.d && !isfinite(comp(g, q))) {
-          flag(p.err, kErrGrad,
-               (static_cast<unsigned long long>(p.worker_base + w) << 40) | k);
+          flag_grad(p, (static_cast<unsigned long long>(p.worker_base + w) << 40) | k);
         }
       }
     }
@@ -603,6 +647,7 @@ __device__ __forceinline__ void k1_tile(const K1Params& p, long long tile, int l
 
 template <int MODE, bool ALIGNED>
 __global__ void __launch_bounds__(kBlock, K1_MINB) k1_worker_compress(const K1Params p) {
+  if (gate_closed_call(p.err)) return;
   __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
   uint32_t* sw = s_words[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -666,8 +711,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 // Bounded wait (a lost completion must never wedge the GPU): gives up after
-// ~2^28 polls, which the parity tests would then catch as wrong output.
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+// ~2^28 polls and closes the gate (kGateInternal), which the host reports.
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase, unsigned long long* err) {
   uint32_t ok = 0;
   for (uint32_t it = 0; it < (1u << 28); ++it) {
     asm volatile(
@@ -677,6 +722,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
         : "memory");
     if (ok) return;
   }
+  close_gate(err, kGateInternal);
 }
 
 __device__ __forceinline__ float4 lds_mis(const float* p, int s) {
@@ -699,6 +745,7 @@ __device__ __forceinline__ int k1_fast_layer(const K1Params& p, int j, int t) {
 
 template <int MODE, int kBulkR>
 __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) {
+  if (gate_closed_call(p.err)) return;
   using Geo = BulkGeom<kBulkR>;
   constexpr int kBulkG = Geo::G, kBulkW = Geo::Wb, kBulkBits = Geo::Bits, kBulkStage = Geo::Stage;
   extern __shared__ __align__(128) unsigned char sm[];
@@ -836,7 +883,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
       acc = 0.0;
       cm = 0.0f;
     }
-    mbar_wait(&bars[wib][stage], phase);
+    mbar_wait(&bars[wib][stage], phase, p.err);
     const unsigned char* st = wsm + stage * kBulkStage;
     const float* gsm = reinterpret_cast<const float*>(st) + s;
     const float* wsm_rows = reinterpret_cast<const float*>(st + kBulkG);
@@ -852,9 +899,8 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (!isfinite(comp(g, q))) {
-            flag(p.err, kErrGrad,
-                 (static_cast<unsigned long long>(p.worker_base + w) << 40) |
-                     (kc + i0 + (cr + k) * kRowElems + 4 * lane + q));
+            flag_grad(p, (static_cast<unsigned long long>(p.worker_base + w) << 40) |
+                             (kc + i0 + (cr + k) * kRowElems + 4 * lane + q));
           }
         }
       }
@@ -931,6 +977,7 @@ __device__ void finalize_commit(const FinalizeParams& p, int e, double s) {
     p.slots[static_cast<size_t>(e) * p.slot_stride + p.W] = __float_as_uint(S);
     if (!isfinite(S)) flag(p.err, kErrScale, static_cast<unsigned long long>(p.err_base + e));
     if (p.peer_slots) {
+      forward_grad_error(p.err, p.peer_err, p.n);  // every rank raises (optimizers.cpp:99-117)
       const int q0 = p.to_all ? 0 : e, q1 = p.to_all ? p.n : e + 1;
       for (int q = q0; q < q1; ++q) p.peer_slots[q][p.peer_off + p.W] = __float_as_uint(S);
       __threadfence_system();  // the scale words before any flag
@@ -940,6 +987,7 @@ __device__ void finalize_commit(const FinalizeParams& p, int e, double s) {
 }
 
 __global__ void __launch_bounds__(1024) k_finalize_scales(const FinalizeParams p) {
+  if (gate_closed_call(p.err)) return;
   __shared__ double sh[32];
   const int e = blockIdx.x;
   const double* part = p.partials + static_cast<size_t>(e) * p.tpc;
@@ -1011,6 +1059,7 @@ __device__ __forceinline__ void flush_server_words(const K3Params& p, uint32_t* 
 #define K3_MINB(NT) ((NT) == 1 ? (K3_R1 == 8 ? 3 : 4) : (NT) == 2 ? K3_B2 : (NT) == 4 ? K3_B4 : (NT) == 8 ? K3_B8 : 2)
 template <int NT>
 __global__ void __launch_bounds__(kBlock, K3_MINB(NT)) k3_server_reduce(const K3Params p) {
+  if (gate_closed_call(p.err)) return;
   __shared__ float s_scale[kWarpsPerBlock][64];
   __shared__ uint32_t* s_peer[64];
   __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
@@ -1030,7 +1079,6 @@ __global__ void __launch_bounds__(kBlock, K3_MINB(NT)) k3_server_reduce(const K3
   const long long total = static_cast<long long>(p.ns) * p.tpc;
   const float es = p.es_dev ? __ldg(p.es_dev) : p.es_host;
   const double inv_n = 1.0 / static_cast<double>(n);
-  if (p.wait_flags) wait_peers(p.wait_flags, n, p.epoch, p.err);
 
   TileSched sch{p.ctr, total, nwarps, 0};
   for (long long tile = sch.first(gw, lane); tile < total; tile = sch.next(lane)) {
@@ -1281,7 +1329,7 @@ __device__ __forceinline__ int lane_valid(uint64_t len, uint64_t ir, int lane) {
 #endif
 template <int MPREV, bool MISK>
 __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p) {
-  if (p.wait_flags) wait_peers(p.wait_flags, p.n, p.epoch, p.err);
+  if (gate_closed_call(p.err)) return;
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -1437,6 +1485,7 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
 // one 1024-thread block per layer; the last block also advances the
 // c_mean history (:328-330) and the experimental error scale (:226-229).
 __global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
+  if (gate_closed_call(p.gate)) return;
   __shared__ double shd[32];
   __shared__ float shf[32];
   __shared__ bool last;
@@ -1500,6 +1549,7 @@ __global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
 // x += (-lr*c)*u, with m_g recomputed from the result packets.
 template <bool MISK>
 __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
+  if (gate_closed_call(p.gate)) return;
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -1590,6 +1640,7 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
 // ---------------------------------------------------------------------------
 template <bool MISK>
 __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
+  if (gate_closed_call(p.gate)) return;
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -1706,6 +1757,7 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
 // Warmup epilogue: per-layer coefficient (optimizers.cpp:158-172) and, at
 // the end of the stage, finalize_warmup (:202-224) in the last block.
 __global__ void __launch_bounds__(1024) k_wepilogue(const WEpiParams p) {
+  if (gate_closed_call(p.gate)) return;
   __shared__ double shd[32];
   __shared__ bool last;
   const int l = blockIdx.x;
@@ -1782,6 +1834,7 @@ __global__ void __launch_bounds__(1024) k_wepilogue(const WEpiParams p) {
 // W2: u = m/(sqrt(v)+eta) [+wd x]; x += (-lr*c)*u; at the freeze vf = v.
 template <bool MISK>
 __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
+  if (gate_closed_call(p.gate)) return;
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
@@ -1856,6 +1909,7 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
 // aligned library buffers), any output alignment.
 __global__ void k_average4(const float* in, uint64_t stride, int n, uint64_t len, float* out,
                            unsigned long long* err, int check, int worker_base) {
+  if (gate_closed_call(err)) return;
   const double inv_n = 1.0 / static_cast<double>(n);
   const uint64_t n4 = len / 4;
   for (uint64_t k4 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k4 < n4;
@@ -1890,6 +1944,7 @@ __global__ void k_average4(const float* in, uint64_t stride, int n, uint64_t len
 
 __global__ void k_average(const float* in, uint64_t stride, int n, uint64_t len, float* out,
                           unsigned long long* err, int check, int worker_base) {
+  if (gate_closed_call(err)) return;
   const double inv_n = 1.0 / static_cast<double>(n);
   for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -1944,8 +1999,7 @@ __device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint
         for (int e = 0; e < 4; ++e) {
           const float x = comp(g[u][q], e);
           if (p.check_finite && !isfinite(x) && k + e < p.d)
-            atomicMin_system(p.peer_err[q0 + q] + kErrGrad,
-                             (static_cast<unsigned long long>(q0 + q) << 40) | (k + e));
+            flag(p.err, kErrGrad, (static_cast<unsigned long long>(q0 + q) << 40) | (k + e));
           a[u][e] += static_cast<double>(x);
         }
       }
@@ -1966,7 +2020,8 @@ __device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint
 #endif
 template <int NT>
 __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p) {
-  wait_peers(p.in_flags, p.n, p.epoch, p.err);  // every rank's gradient is in place
+  if (gate_closed_call(p.err)) return;
+  if (!wait_peers(p.in_flags, p.n, p.epoch, p.err)) return;  // every rank's gradient is in place
   const double inv_n = 1.0 / static_cast<double>(p.n);
   const uint64_t lo = static_cast<uint64_t>(p.rank) * p.c, hi = lo + p.c;
   const uint64_t up = (lo + 3) & ~3ull, dn = hi & ~3ull;  // 16-B aligned body [a0, a1)
@@ -1985,7 +2040,7 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
       for (int q = 0; q < p.n; ++q) {
         const float x = __ldcg(p.peer_in[q] + k);
         if (p.check_finite && !isfinite(x) && k < p.d)
-          atomicMin_system(p.peer_err[q] + kErrGrad, (static_cast<unsigned long long>(q) << 40) | k);
+          flag(p.err, kErrGrad, (static_cast<unsigned long long>(q) << 40) | k);
         acc += static_cast<double>(x);
       }
       const float v = static_cast<float>(acc * inv_n);
@@ -1996,13 +2051,16 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
   __syncthreads();
   if (threadIdx.x == 0 && atomicAdd(p.done, 1u) == gridDim.x - 1) {
     *p.done = 0u;
+    __threadfence();
+    forward_grad_error(p.err, p.peer_err, p.n);  // every rank raises (optimizers.cpp:99-117)
     __threadfence_system();
     for (int q = 0; q < p.n; ++q) st_relaxed_sys(p.peer_flags[q] + p.out_flag + p.rank, p.epoch);
   }
 }
 
 __global__ void k_signal_peers(unsigned long long* const* peer_flags, int index, int n,
-                               unsigned long long epoch) {
+                               unsigned long long epoch, const unsigned long long* gate) {
+  if (gate_closed_call(gate)) return;
   if (threadIdx.x == 0) {
     __threadfence_system();
     for (int q = 0; q < n; ++q) st_relaxed_sys(peer_flags[q] + index, epoch);
@@ -2034,7 +2092,8 @@ __device__ __forceinline__ void decompress_warps(const uint32_t* res, int n, uin
 }
 
 __global__ void k_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
-                             uint64_t d, float* out) {
+                             uint64_t d, float* out, const unsigned long long* gate) {
+  if (gate_closed_call(gate)) return;
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   decompress_warps(res, n, c, slot, W, d, out, gw, nwarps, threadIdx.x & 31);
@@ -2048,7 +2107,8 @@ __global__ void k_decompress(const uint32_t* res, int n, uint64_t c, uint64_t sl
 // separated by grid barriers and the peers' epoch flags only.  Every
 // per-element operation and reduction order is the unfused path's.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks,
+                                             unsigned long long* err) {
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned int* gen = bar + 1;
@@ -2061,6 +2121,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
     } else {
       long long spins = 0;
       while (*gen == g && ++spins < (1ll << 30)) __nanosleep(32);
+      if (*gen == g) close_gate(err, kGateInternal);  // co-residency broken: fail-stop
     }
     __threadfence();
   }
@@ -2140,8 +2201,8 @@ __device__ __forceinline__ void k1_cta_tile(const K1Params& p, long long tile, u
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (!isfinite(comp(g[k], q)))
-          flag(p.err, kErrGrad, (static_cast<unsigned long long>(p.worker_base + w) << 40) |
-                                    (kc + i0 + (r0 + k) * kRowElems + 4 * lane + q));
+          flag_grad(p, (static_cast<unsigned long long>(p.worker_base + w) << 40) |
+                           (kc + i0 + (r0 + k) * kRowElems + 4 * lane + q));
     }
     uint32_t nib = 0;
     float4 rawn, ab;
@@ -2295,6 +2356,7 @@ __global__ void __launch_bounds__(kBlock) k_small_collective(__grid_constant__ c
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  if (gate_closed_call(p.err)) return;  // every CTA: the grid barriers stay balanced
   const int n = p.k1.n;
   for (int q = threadIdx.x; q < n; q += blockDim.x) s_peer[q] = p.k3.peer_res[q];
   // 1. worker compression of every chunk of the local stream; packet words
@@ -2306,14 +2368,15 @@ __global__ void __launch_bounds__(kBlock) k_small_collective(__grid_constant__ c
       k1_cta_tile<MODE, ALIGNED>(p.k1, tile, s_words, s_abs, s_cm, es);
     warp_fence_system(lane);
   }
-  grid_barrier(p.bar, gridDim.x);
+  grid_barrier(p.bar, gridDim.x, p.err);
   // 2. worker scales: block e finalizes endpoint (this worker, chunk e) and
   //    raises rank e's flag
   for (int e = blockIdx.x; e < n; e += gridDim.x) finalize_block256(p.f1, e, s_red);
-  // 3. every worker's packet for this rank's chunk has arrived
-  wait_peers(p.flags, n, p.epoch, p.err);
+  // 3. every worker's packet for this rank's chunk has arrived (a peer
+  //    timeout closes the gate: the rest is skipped, the barriers still run)
+  const bool live = wait_peers(p.flags, n, p.epoch, p.err);
   // 4. server reduce of chunk `rank`; server words into every rank's result slot
-  {
+  if (live) {
     const float es = p.k3.es_dev ? __ldg(p.k3.es_dev) : p.k3.es_host;
     const double inv_n = 1.0 / static_cast<double>(n);
     for (int i = threadIdx.x; i < n; i += blockDim.x) s_scale[i] = slot_scale_cg(p.k3.in + i * p.k3.in_i, p.k3.W);
@@ -2322,12 +2385,11 @@ __global__ void __launch_bounds__(kBlock) k_small_collective(__grid_constant__ c
       k3_cta_tile(p.k3, tile, s_words, s_abs, s_cm, s_scale, s_peer, es, inv_n);
     warp_fence_system(lane);
   }
-  grid_barrier(p.bar, gridDim.x);
+  grid_barrier(p.bar, gridDim.x, p.err);
   // 5. server scale to every rank, flags
-  if (blockIdx.x == 0) finalize_block256(p.f2, 0, s_red);
+  if (live && blockIdx.x == 0) finalize_block256(p.f2, 0, s_red);
   // 6. every rank's server packet has arrived; 7. optional decompress
-  wait_peers(p.flags + n, n, p.epoch, p.err);
-  if (p.out)
+  if (live && wait_peers(p.flags + n, n, p.epoch, p.err) && p.out)
     decompress_warps(p.res, n, p.k3.c, p.k3.slot, p.k3.W, p.d, p.out, static_cast<uint64_t>(gw),
                      static_cast<uint64_t>(nwarps), lane);
 }
@@ -2416,6 +2478,7 @@ __global__ void k_set_float(float* p, float v) { *p = v; }
 
 __global__ void k_verify(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot,
                          uint64_t W, uint64_t c, uint64_t len, double tol, unsigned long long* err) {
+  if (gate_closed_call(err)) return;
   for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < len;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t j = k / c, i = k - j * c;
@@ -2436,12 +2499,200 @@ __global__ void k_verify(const float* raw, uint64_t c_pad, const uint32_t* pk, u
 // Stream-ordered wait for n peer signals (fused NVLink exchange).
 __global__ void k_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
                              unsigned long long* err) {
+  if (gate_closed_call(err)) return;
   wait_peers(flags, n, epoch, err);
+}
+
+// ---------------------------------------------------------------------------
+// Step gate.  check_gradients (optimizers.cpp:99-117) validates every worker's
+// gradient before any state changes; strict mode restates that with a
+// read-only pre-pass (k_check_finite) whose finding closes the gate before the
+// first mutating kernel.  Multi-process, the gate kernel is also the step's
+// arrival barrier, so a rank that is late past the bound aborts the step on
+// every rank before anything is written (fail-stop, state unchanged).
+// ---------------------------------------------------------------------------
+__global__ void k_check_finite(const float* in, uint64_t stride, int nw, uint64_t d,
+                               unsigned long long* err, int worker_base) {
+  if (gate_closed_call(err)) return;
+  const uint64_t d4 = d / 4;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (int w = 0; w < nw; ++w) {
+    const float* g = in + static_cast<size_t>(w) * stride;
+    const unsigned long long wk = static_cast<unsigned long long>(worker_base + w) << 40;
+    for (uint64_t k4 = tid; k4 < d4; k4 += nth) {
+      const float4 v = ldg_ro(g + 4 * k4);
+      if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w))) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (!isfinite(comp(v, q))) flag(err, kErrGrad, wk | (4 * k4 + q));
+      }
+    }
+    for (uint64_t k = 4 * d4 + tid; k < d; k += nth)
+      if (!isfinite(g[k])) flag(err, kErrGrad, wk | k);
+  }
+}
+
+__device__ __forceinline__ unsigned long long local_nonfinite_layer(const unsigned long long* err,
+                                                                   const uint64_t* off, int L) {
+  const unsigned long long key = ld_volatile_u64(err + kErrGrad);
+  if (key == ~0ull) return 0;  // finite
+  const uint64_t k = key & ((1ull << 40) - 1);
+  return (off ? static_cast<unsigned long long>(find_layer(off, L, k)) : 0ull) + 1;  // layer + 1
+}
+
+__global__ void k_step_gate(const GateParams p) {
+  if (threadIdx.x != 0) return;
+  unsigned long long* err = p.err;
+  if (gate_closed_call(err)) return;  // an earlier failure is still unreported: this step is skipped too
+  const unsigned long long status = p.strict ? local_nonfinite_layer(err, p.off, p.L) : 0;
+  if (p.peer_flags == nullptr || p.n == 1) {
+    if (status) {
+      atomicMin(err + kErrGateSeq, p.seq);
+      close_gate(err, kGateNonFinite);
+    }
+    return;
+  }
+  // Arrival: (epoch << 32) | status, into every rank's arrival word of this rank.
+  const unsigned long long mine = (p.epoch << 32) | (status & 0xffffffffull);
+  for (int q = 0; q < p.n; ++q) st_relaxed_sys(p.peer_flags[q] + p.arrive_index + p.rank, mine);
+  const unsigned long long bound = wait_bound(err), t0 = now_ns();
+  int missing = -1;
+  for (int q = 0; q < p.n && missing < 0; ++q) {
+    while ((ld_acquire_sys(p.arrive + q) >> 32) < p.epoch) {
+      if (now_ns() - t0 > bound) {
+        missing = q;
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  // One decision per epoch, CAS-ed into rank 0's word: the first rank to
+  // decide (go: all arrived / abort: someone missing) decides for everyone.
+  unsigned long long* dec = p.peer_flags[0] + p.decision_index;
+  const unsigned long long want =
+      (p.epoch << 32) | (missing < 0 ? (1ull << 16) : ((2ull << 16) | static_cast<unsigned>(missing)));
+  unsigned long long cur = ld_acquire_sys(dec), decided = want;
+  while (true) {
+    if ((cur >> 32) == p.epoch) {
+      decided = cur;
+      break;
+    }
+    const unsigned long long prev = atomicCAS_system(dec, cur, want);
+    if (prev == cur) break;  // ours
+    cur = prev;
+  }
+  if (((decided >> 16) & 0xffffull) != 1ull) {  // abort: nobody touches the state
+    flag(err, kErrPeer, decided & 0xffffull);
+    atomicMin(err + kErrGateSeq, p.seq);
+    close_gate(err, kGateArrival);
+    return;
+  }
+  // Go: every rank arrived; the lowest rank with a non-finite gradient is
+  // reported by every rank (the arrivals are all posted, so this terminates).
+  for (int q = 0; q < p.n; ++q) {
+    unsigned long long a;
+    while (((a = ld_acquire_sys(p.arrive + q)) >> 32) < p.epoch) __nanosleep(32);
+    const unsigned long long st = a & 0xffffffffull;
+    if (st != 0 && (a >> 32) == p.epoch) {
+      flag(err, kErrRemote, (static_cast<unsigned long long>(q) << 32) | (st - 1));
+      atomicMin(err + kErrGateSeq, p.seq);
+      close_gate(err, q == p.rank ? kGateNonFinite : kGateRemoteNonFinite);
+      return;
+    }
+  }
+}
+
+// NCCL transport: status word = rank << 32 | layer of this rank's first
+// non-finite element (strict pre-pass), ~0 if finite; min-reduced over ranks.
+__global__ void k_gate_status(unsigned long long* err, const uint64_t* off, int L, int rank,
+                              unsigned long long* status) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long st = gate_closed(err) ? 0ull : local_nonfinite_layer(err, off, L);
+  *status = st ? (static_cast<unsigned long long>(rank) << 32) | (st - 1) : ~0ull;
+}
+
+__global__ void k_gate_apply(unsigned long long* err, const unsigned long long* status, int rank,
+                             unsigned long long seq) {
+  if (threadIdx.x != 0 || gate_closed(err)) return;
+  const unsigned long long st = *status;
+  if (st == ~0ull) return;
+  flag(err, kErrRemote, st);
+  atomicMin(err + kErrGateSeq, seq);
+  close_gate(err, static_cast<int>(st >> 32) == rank ? kGateNonFinite : kGateRemoteNonFinite);
+}
+
+// ---------------------------------------------------------------------------
+// Free functions of fusion.hpp:92-102 (compute_scales, apply/remove_scaling).
+// ---------------------------------------------------------------------------
+// Per-layer tile partials of |x| in the canonical tile-tree order (oracle
+// tile_partial), one warp per tile.
+__global__ void k_layer_abs_tiles(const float* x, const uint64_t* off, const int* tile_layer,
+                                  const int* layer_tile_start, int tiles, double* part) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  for (long long tile = gw; tile < tiles; tile += nwarps) {
+    const int l = tile_layer[tile];
+    const uint64_t t = static_cast<uint64_t>(tile - layer_tile_start[l]);
+    const uint64_t lo = off[l], len = off[l + 1] - lo;
+    double acc = 0.0;
+    for (int r = 0; r < kRowsPerTile; ++r)
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t i = t * kTile + static_cast<uint64_t>(r) * kRowElems + 4 * lane + q;
+        if (i < len) acc += fabs(static_cast<double>(x[lo + i]));
+      }
+    acc = warp_bfly_sum(acc);
+    if (lane == 0) part[tile] = acc;
+  }
+}
+
+// compute_scales (fusion.cpp:107-125): block l combines its layer's partials
+// (k_finalize_scales' order), s_l = max(sum / len, floor); the last block forms
+// reference = (sum_l s_l) / L in layer order and coeff_l = reference / s_l.
+__global__ void __launch_bounds__(1024) k_scales_final(int L, const int* layer_tile_start,
+                                                       const uint64_t* off, const double* part,
+                                                       double floor_, double* mag, double* coeff,
+                                                       double* ref_out, unsigned int* counter) {
+  __shared__ double sh[32];
+  __shared__ bool last;
+  const int l = blockIdx.x;
+  double s = stripe_sum(part, layer_tile_start[l] + threadIdx.x, layer_tile_start[l + 1]);
+  s = block1024_sum(s, sh);
+  if (threadIdx.x == 0) {
+    const uint64_t len = off[l + 1] - off[l];
+    const double mean = len == 0 ? 0.0 : s / static_cast<double>(len);  // vector_ops.cpp:41-44
+    mag[l] = mean < floor_ ? floor_ : mean;                            // fusion.cpp:116
+    __threadfence();
+    last = atomicAdd(counter, 1u) == static_cast<unsigned>(L - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* m = mag;
+    double ref = 0.0;
+    for (int k = 0; k < L; ++k) ref += m[k];  // fusion.cpp:118-120
+    ref /= static_cast<double>(L);
+    for (int k = 0; k < L; ++k) coeff[k] = ref / m[k];  // :121-124
+    *ref_out = ref;
+    *counter = 0u;
+  }
+}
+
+// apply_scaling / remove_scaling (fusion.cpp:127-149): x[k] *= mul[layer(k)],
+// mul = (float)coeff or (float)(1.0 / coeff) formed in double once per layer.
+__global__ void k_scale_layers(float* x, const uint64_t* off, int L, const float* mul, uint64_t d) {
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < d;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int l = find_layer(off, L, k);
+    x[k] = __fmul_rn(x[k], __ldg(mul + l));
+  }
 }
 
 __global__ void k_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const float* m,
                                const uint64_t* off, int L, const float* A, const float* B,
                                unsigned long long* err, int worker_base) {
+  if (gate_closed_call(err)) return;
   for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < d;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int l = find_layer(off, L, k);
@@ -2630,8 +2881,8 @@ int launch_average(const float* in, uint64_t stride, int n, uint64_t len, float*
 }
 
 int launch_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
-                      uint64_t d, float* out, cudaStream_t s) {
-  k_decompress<<<grid_for_elems(d / 128 + 1), 256, 0, s>>>(res, n, c, slot, W, d, out);
+                      uint64_t d, float* out, const unsigned long long* gate, cudaStream_t s) {
+  k_decompress<<<grid_for_elems(d / 128 + 1), 256, 0, s>>>(res, n, c, slot, W, d, out, gate);
   return 1;
 }
 
@@ -2706,14 +2957,57 @@ int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s) {
 }
 
 int launch_signal_peers(unsigned long long* const* peer_flags, int index, int n,
-                        unsigned long long epoch, cudaStream_t s) {
-  k_signal_peers<<<1, 32, 0, s>>>(peer_flags, index, n, epoch);
+                        unsigned long long epoch, const unsigned long long* gate, cudaStream_t s) {
+  k_signal_peers<<<1, 32, 0, s>>>(peer_flags, index, n, epoch, gate);
   return 1;
 }
 
 int launch_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
                       unsigned long long* err, cudaStream_t s) {
   k_wait_peers<<<1, 32, 0, s>>>(flags, n, epoch, err);
+  return 1;
+}
+
+int launch_layer_abs_tiles(const float* x, const uint64_t* off, const int* tile_layer,
+                           const int* layer_tile_start, int tiles, double* part, cudaStream_t s) {
+  const int g = (tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  k_layer_abs_tiles<<<g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16, kBlock, 0, s>>>(x, off, tile_layer,
+                                                                                layer_tile_start, tiles, part);
+  return 1;
+}
+
+int launch_scales_final(int L, const int* layer_tile_start, const uint64_t* off, const double* part,
+                        double floor_, double* mag, double* coeff, double* ref_out, unsigned int* counter,
+                        cudaStream_t s) {
+  k_scales_final<<<L, 1024, 0, s>>>(L, layer_tile_start, off, part, floor_, mag, coeff, ref_out, counter);
+  return 1;
+}
+
+int launch_scale_layers(float* x, const uint64_t* off, int L, const float* mul, uint64_t d, cudaStream_t s) {
+  k_scale_layers<<<grid_for_elems(d), 256, 0, s>>>(x, off, L, mul, d);
+  return 1;
+}
+
+int launch_check_finite(const float* in, uint64_t stride, int nw, uint64_t d, unsigned long long* err,
+                        int worker_base, cudaStream_t s) {
+  k_check_finite<<<grid_for_elems(d / 4 + 1), 256, 0, s>>>(in, stride, nw, d, err, worker_base);
+  return 1;
+}
+
+int launch_step_gate(const GateParams& p, cudaStream_t s) {
+  k_step_gate<<<1, 32, 0, s>>>(p);
+  return 1;
+}
+
+int launch_gate_status(unsigned long long* err, const uint64_t* off, int L, int rank,
+                       unsigned long long* status, cudaStream_t s) {
+  k_gate_status<<<1, 32, 0, s>>>(err, off, L, rank, status);
+  return 1;
+}
+
+int launch_gate_apply(unsigned long long* err, const unsigned long long* status, int rank,
+                      unsigned long long seq, cudaStream_t s) {
+  k_gate_apply<<<1, 32, 0, s>>>(err, status, rank, seq);
   return 1;
 }
 

@@ -20,14 +20,30 @@ constexpr int kRowsPerTile = 32;
 constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 256;
 
-// Device error words (atomicMin keys, ~0ull = none).
+// Device error words (atomicMin keys, ~0ull = none), then configuration words.
 enum ErrSlot : int {
-  kErrGrad = 0,    // non-finite gradient: key = worker << 40 | element
-  kErrScale = 1,   // non-finite compression scale: key = endpoint id
-  kErrRecon = 2,   // non-finite reconstructed gradient: key = layer
-  kErrPeer = 3,    // peer signal timeout (fused NVLink exchange): key = peer rank
-  kErrVerify = 4,  // compensation identity violated: key = chunk-relative element
-  kErrSlots = 5,
+  kErrGrad = 0,     // non-finite gradient: key = worker << 40 | element
+  kErrScale = 1,    // non-finite compression scale: key = endpoint id
+  kErrRecon = 2,    // non-finite reconstructed gradient: key = layer
+  kErrPeer = 3,     // peer timeout: key = peer rank
+  kErrVerify = 4,   // compensation identity violated: key = chunk-relative element
+  kErrGate = 5,     // step gate: ~0 open, else the GateReason that closed it
+  kErrGateSeq = 6,  // host sequence number of the step/collective the gate closed at
+  kErrRemote = 7,   // non-finite gradient reported by a peer: rank << 32 | layer
+  kErrSlots = 8,    // error words (reset to ~0 by the host after it reports them)
+  kCfgTimeout = 8,  // peer wait bound in ns (configuration, never reset)
+  kErrWords = 16,
+};
+
+// Why the step gate closed.  While it is closed every mutating kernel of the
+// cluster returns at entry, so the rest of the step (and any step enqueued
+// after it) leaves the state untouched until the host reports the error.
+enum GateReason : unsigned long long {
+  kGateNonFinite = 1,        // strict pre-pass: this rank's gradient is not finite (no mutation yet)
+  kGateRemoteNonFinite = 2,  // a peer's strict pre-pass failed (no mutation yet)
+  kGateArrival = 3,          // a peer did not arrive at the step within the timeout (no mutation yet)
+  kGateMidStep = 4,          // a peer stopped signalling inside a step: fail-stop, state undefined
+  kGateInternal = 5,         // a device-side barrier timed out: fail-stop
 };
 
 // K1: worker compression of `nw` local streams, each split into n chunks.
@@ -87,10 +103,8 @@ struct K3Params {
   float es_host;
   double* partials;           // [ns][tpc]
   float* cmax;                // [ns][tpc] or nullptr
-  // Fused NVLink exchange: wait for every worker's packet, then store the
-  // server words into every peer's result slot peer_res[q] + res_off.
-  const unsigned long long* wait_flags;  // [n] local worker flags or nullptr
-  unsigned long long epoch;
+  // Fused NVLink exchange: the server words also go into every peer's result
+  // slot peer_res[q] + res_off (the stream waited for the packets before).
   uint32_t* const* peer_res;  // [n] peer result-buffer bases or nullptr
   uint64_t res_off;
   int rank;
@@ -116,6 +130,7 @@ struct FinalizeParams {
   int to_all;
   int n;
   unsigned long long epoch;
+  unsigned long long* const* peer_err;  // [n] forward a local kErrGrad finding to every rank
 };
 
 // Layer-tiled kernels (K5, K6, W1, W2).
@@ -147,11 +162,10 @@ struct K5Params {
   const float* dense;        // identity compressor: dense result (m_g = dense * invc)
   float* m_store;            // identity compressor: m <- m_g
   int norm_only;             // lamb_basic_1bit / onebit_adam: only ||v||^2 partials
-  const unsigned long long* wait_flags;  // [n] server flags (fused exchange) or nullptr
-  unsigned long long epoch;
 };
 
 struct EpiParams {
+  const unsigned long long* gate;  // cluster error words (kErrGate)
   int L;
   const int* layer_tile_start;
   const float* tile_max;
@@ -169,6 +183,7 @@ struct EpiParams {
 };
 
 struct K6Params {
+  const unsigned long long* gate;
   LayerTiles lt;
   int n;
   uint64_t c, slot, W;
@@ -212,6 +227,7 @@ struct LosslessP2PParams {
 };
 
 struct W1Params {
+  const unsigned long long* gate;
   LayerTiles lt;
   const float* gbar;
   float *m, *v;
@@ -224,6 +240,7 @@ struct W1Params {
 };
 
 struct WEpiParams {
+  const unsigned long long* gate;
   int L;
   const int* layer_tile_start;
   const uint64_t* off;
@@ -242,6 +259,7 @@ struct WEpiParams {
 };
 
 struct W2Params {
+  const unsigned long long* gate;
   LayerTiles lt;
   const float *m, *v;
   float* x;
@@ -249,6 +267,24 @@ struct W2Params {
   const float* coef_x;
   float eta, wd;
   int finalize;
+};
+
+// Step gate (start of every step / collective).  Strict mode: a non-finite
+// local gradient found by the pre-pass closes the gate.  Multi-process (P2P):
+// every rank posts its arrival (epoch, status) into every peer's flag words
+// and waits for all arrivals within the timeout; a go/abort decision is
+// CAS-ed once into rank 0's decision word, so every rank takes the same one.
+struct GateParams {
+  unsigned long long* err;                 // local error words
+  unsigned long long seq;                  // host sequence number (rollback key)
+  unsigned long long epoch;                // barrier epoch (same on every rank)
+  int n, rank, strict;
+  unsigned long long* const* peer_flags;   // [n] every rank's flag words (nullptr: local only)
+  const unsigned long long* arrive;        // local arrival words [n]
+  int arrive_index;                        // flag index of arrival word 0
+  int decision_index;                      // flag index of the decision word (rank 0's is used)
+  const uint64_t* off;                     // layer table [L+1] (layer of a non-finite element)
+  int L;
 };
 
 // Host launchers (bl_kernels.cu).  Each returns the number of kernels launched.
@@ -270,7 +306,7 @@ int launch_average(const float* in, uint64_t stride, int n, uint64_t len, float*
                    unsigned long long* err, int check_finite, int worker_base, cudaStream_t s);
 // out[k] (k < d) = decompressed result of packets res[n][slot].
 int launch_decompress(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
-                      uint64_t d, float* out, cudaStream_t s);
+                      uint64_t d, float* out, const unsigned long long* gate, cudaStream_t s);
 // out[k] (k < len) = raw[j][i] - (bit ? S : -S) for flat k = j*c + i; pk [nch][slot].
 int launch_materialize_error(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot,
                              uint64_t W, uint64_t c, uint64_t len, float* out, cudaStream_t s);
@@ -296,9 +332,27 @@ int launch_small_collective(const SmallParams& p, int k1_mode, cudaStream_t s);
 // Raise flag `index` (+ own rank) at every peer to `epoch` after this stream's
 // prior work (system-scope release).
 int launch_signal_peers(unsigned long long* const* peer_flags, int index, int n,
-                        unsigned long long epoch, cudaStream_t s);
+                        unsigned long long epoch, const unsigned long long* gate, cudaStream_t s);
 int launch_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
                       unsigned long long* err, cudaStream_t s);
+// Strict pre-pass (optimizers.cpp:99-117, before any mutation): flags the
+// first non-finite element of the nw local gradients in kErrGrad.
+int launch_check_finite(const float* in, uint64_t stride, int nw, uint64_t d, unsigned long long* err,
+                        int worker_base, cudaStream_t s);
+int launch_step_gate(const GateParams& p, cudaStream_t s);
+// fusion.hpp:92-102 free functions on the device.
+int launch_layer_abs_tiles(const float* x, const uint64_t* off, const int* tile_layer,
+                           const int* layer_tile_start, int tiles, double* part, cudaStream_t s);
+int launch_scales_final(int L, const int* layer_tile_start, const uint64_t* off, const double* part,
+                        double floor_, double* mag, double* coeff, double* ref_out, unsigned int* counter,
+                        cudaStream_t s);
+int launch_scale_layers(float* x, const uint64_t* off, int L, const float* mul, uint64_t d, cudaStream_t s);
+// NCCL transport: this rank's gate status as one word (min-reduced over the
+// ranks by ncclAllReduce between the two launches), then applied.
+int launch_gate_status(unsigned long long* err, const uint64_t* off, int L, int rank,
+                       unsigned long long* status, cudaStream_t s);
+int launch_gate_apply(unsigned long long* err, const unsigned long long* status, int rank,
+                      unsigned long long seq, cudaStream_t s);
 // Identity-compressor stream build in place (optimizers.cpp:248-255):
 // in[w][k] = A_l*m[k] + B_l*in[w][k] for k < d, with the gradient finite check.
 int launch_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const float* m,

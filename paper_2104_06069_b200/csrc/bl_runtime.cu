@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 
 namespace bl {
@@ -25,7 +26,7 @@ const char* const kClassNames[KC_COUNT] = {
     "layer_epilogue",     "k6_update_b",     "w1_warmup_a",      "warmup_epilogue",
     "w2_warmup_b",        "average",         "decompress",       "materialize",
     "endpoint_stats",     "nccl_alltoall",   "nccl_allgather",   "h2d_copy",
-    "d2h_copy",           "k1_boundary_tiles", "small_collective"};
+    "d2h_copy",           "k1_boundary_tiles", "small_collective", "step_gate"};
 
 void fail(bl_status st, const std::string& msg) { throw Error{st, msg}; }
 
@@ -222,6 +223,7 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
     sp.f1.to_all = 0;
     sp.f1.n = n;
     sp.f1.epoch = epoch;
+    sp.f1.peer_err = d_peer_err;
     K3Params& k3 = sp.k3;
     k3.n = n;
     k3.ns = 1;
@@ -327,6 +329,7 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
     f.to_all = 0;
     f.n = n;
     f.epoch = epoch;
+    f.peer_err = d_peer_err;  // a non-finite gradient is reported to every rank
   }
   begin(KC_FIN, &a);
   end(KC_FIN, a, launch_finalize(f, nw * n, stream));
@@ -433,7 +436,7 @@ void bl_cluster::finish_compressed(float es_host, const float* es_dev) {
 void bl_cluster::setup_p2p(bool required) {
   const size_t nn = static_cast<size_t>(n);
   rx = dalloc<uint32_t>(2 * nn * slot);
-  flags = reinterpret_cast<unsigned long long*>(dalloc<double>(4 * nn));
+  flags = reinterpret_cast<unsigned long long*>(dalloc<double>(5 * nn + 8));
   lossless_done = reinterpret_cast<unsigned int*>(dalloc<float>(1));
   small_bar = reinterpret_cast<unsigned int*>(dalloc<float>(2));
   // Buffers every peer maps: packet receive slots, result packets, flags,
@@ -517,7 +520,7 @@ void bl_cluster::lossless(bool check_finite) {
     const unsigned long long ep = ++lcalls;
     const int nn = n;
     begin(KC_A2A, &a);
-    end(KC_A2A, a, launch_signal_peers(d_peer_flags, 2 * nn + rank, nn, ep, stream));
+    end(KC_A2A, a, launch_signal_peers(d_peer_flags, 2 * nn + rank, nn, ep, err, stream));
     LosslessP2PParams lp{};
     lp.peer_in = d_peer_in;
     lp.peer_out = d_peer_out;
@@ -644,27 +647,181 @@ void bl_cluster::refresh_stats() {  // comm_sim.cpp:108-118, 175-180
   }
 }
 
-void bl_cluster::check_errors(const std::vector<uint64_t>* off) {
+namespace {
+std::string layer_label(const bl_optimizer* opt, long long layer) {
+  if (opt && layer >= 0 && layer < static_cast<long long>(opt->names.size()))
+    return opt->names[static_cast<size_t>(layer)];
+  return "layer" + std::to_string(layer);
+}
+long long layer_of(const bl_optimizer* opt, uint64_t k) {
+  if (!opt) return -1;
+  return std::upper_bound(opt->off.begin(), opt->off.end(), k) - opt->off.begin() - 1;
+}
+}  // namespace
+
+void bl_cluster::ensure_usable() const {
+  if (broken) fail(BL_ERR_NCCL, "cluster failed earlier and its state is undefined: " + broken_msg);
+}
+
+void bl_cluster::begin_step(bl_optimizer* opt, uint64_t t, bool is_step, bool strict_check) {
+  ensure_usable();
+  seq += 1;
+  Snap sn{};
+  sn.seq = seq;
+  sn.t = t;
+  sn.is_step = is_step;
+  sn.calls = calls;
+  sn.checks = checks;
+  sn.last_identity = last_identity;
+  sn.ledger = ledger;
+  sn.opt = opt;
+  if (opt) {
+    sn.frozen = opt->frozen;
+    sn.has_vf = opt->has_vf;
+    sn.has_mprev = opt->has_mprev;
+    sn.m_valid = opt->m_valid;
+    sn.mprev_separate = opt->mprev_separate;
+    sn.my_calls = opt->my_calls;
+  }
+  if (snaps.size() >= 4096) snaps.erase(snaps.begin());  // unsynchronized for that long: keep the tail
+  snaps.push_back(sn);
+
+  const bool multi = mode == BL_MODE_NCCL && n > 1;
+  if (!strict_check && !multi) return;
+  cudaEvent_t a;
+  if (strict_check) {  // check_gradients (optimizers.cpp:99-117) before any mutation
+    begin(KC_GATE, &a);
+    end(KC_GATE, a, launch_check_finite(in, in_stride, nw, dim, err, mode == BL_MODE_SIM ? 0 : rank, stream));
+  }
+  const uint64_t* off_dev = opt ? opt->off_dev : nullptr;
+  const int L = opt ? opt->L : 0;
+  if (multi && transport != BL_TRANSPORT_P2P) {
+    // NCCL transport: waits without a bound (NCCL's own semantics); only the
+    // strict finding travels, as a min-reduced status word.
+    if (!strict_check) return;
+    if (!gate_status) gate_status = reinterpret_cast<unsigned long long*>(dalloc<double>(1));
+    begin(KC_GATE, &a);
+    end(KC_GATE, a, launch_gate_status(err, off_dev, L, rank, gate_status, stream));
+    nccl_check(ncclAllReduce(gate_status, gate_status, 1, ncclUint64, ncclMin, comm, stream),
+               "ncclAllReduce(gate)");
+    begin(KC_GATE, &a);
+    end(KC_GATE, a, launch_gate_apply(err, gate_status, rank, seq, stream));
+    return;
+  }
+  GateParams g{};
+  g.err = err;
+  g.seq = seq;
+  g.epoch = ++gate_epoch;
+  g.n = multi ? n : 1;
+  g.rank = rank;
+  g.strict = strict_check ? 1 : 0;
+  g.peer_flags = multi ? d_peer_flags : nullptr;
+  g.arrive = flags ? flags + 4 * n : nullptr;
+  g.arrive_index = 4 * n;
+  g.decision_index = 5 * n;
+  g.off = off_dev;
+  g.L = L;
+  begin(KC_GATE, &a);
+  end(KC_GATE, a, launch_step_gate(g, stream));
+}
+
+void bl_cluster::set_peer_timeout(double ms) {
+  peer_timeout_ms = ms;
+  const unsigned long long ns = static_cast<unsigned long long>(ms * 1e6);
+  cuda_check(cudaMemcpy(err + kCfgTimeout, &ns, sizeof ns, cudaMemcpyHostToDevice), "peer timeout");
+}
+
+void bl_cluster::rollback(uint64_t seq_closed) {
+  auto it = std::find_if(snaps.begin(), snaps.end(), [&](const Snap& s) { return s.seq == seq_closed; });
+  if (it == snaps.end()) {
+    broken = true;
+    broken_msg = "a step was aborted on the device but its host snapshot is gone";
+    return;
+  }
+  calls = it->calls;
+  checks = it->checks;
+  last_identity = it->last_identity;
+  ledger = it->ledger;
+  if (bl_optimizer* o = it->opt) {
+    o->frozen = it->frozen;
+    o->has_vf = it->has_vf;
+    o->has_mprev = it->has_mprev;
+    o->m_valid = it->m_valid;
+    o->mprev_separate = it->mprev_separate;
+    o->my_calls = it->my_calls;
+  }
+  snaps.clear();
+}
+
+void bl_cluster::check_errors(const bl_optimizer* opt) {
+  if (!opt) opt = last_opt;
   unsigned long long e[kErrSlots];
   cuda_check(cudaMemcpy(e, err, sizeof e, cudaMemcpyDeviceToHost), "error words");
   const unsigned long long none = ~0ull;
   bool any = false;
   for (int k = 0; k < kErrSlots; ++k) any |= e[k] != none;
-  if (!any) return;
+  if (!any) {
+    snaps.clear();  // everything enqueued so far completed cleanly
+    return;
+  }
   cuda_check(cudaMemset(err, 0xFF, sizeof e), "reset error words");
-  char buf[256];
-  if (e[kErrGrad] != none) {  // optimizers.cpp:109-114
+  char buf[512];
+  if (e[kErrGate] != none) {
+    const unsigned long long reason = e[kErrGate];
+    uint64_t t = pending_step;
+    const bl_optimizer* o = opt;
+    for (const Snap& sn : snaps)
+      if (sn.seq == e[kErrGateSeq]) {
+        t = sn.t;
+        if (sn.opt) o = sn.opt;
+      }
+    if (reason == kGateNonFinite || reason == kGateRemoteNonFinite) {
+      // optimizers.cpp:109-114, raised before anything changed (strict mode)
+      unsigned long long worker = 0;
+      long long layer = -1;
+      if (e[kErrRemote] != none) {
+        worker = e[kErrRemote] >> 32;
+        layer = static_cast<long long>(e[kErrRemote] & 0xffffffffull);
+      } else if (e[kErrGrad] != none) {
+        worker = e[kErrGrad] >> 40;
+        layer = layer_of(o, e[kErrGrad] & ((1ull << 40) - 1));
+      }
+      rollback(e[kErrGateSeq]);
+      std::snprintf(buf, sizeof buf, "non-finite gradient at step %" PRIu64 ", worker %llu, layer '%s'", t,
+                    worker, layer_label(o, layer).c_str());
+      fail(BL_ERR_RUNTIME, buf);
+    }
+    if (reason == kGateArrival) {
+      rollback(e[kErrGateSeq]);
+      std::snprintf(buf, sizeof buf,
+                    "rank %llu did not reach step %" PRIu64 " within %.0f ms: the step was aborted on every "
+                    "rank before any state changed",
+                    e[kErrPeer], t, peer_timeout_ms);
+      fail(BL_ERR_NCCL, buf);
+    }
+    broken = true;
+    if (reason == kGateMidStep) {
+      std::snprintf(buf, sizeof buf,
+                    "rank %llu stopped signalling inside a step (no flag for %.0f ms): fail-stop, the "
+                    "cluster state is undefined",
+                    e[kErrPeer], peer_timeout_ms);
+    } else {
+      std::snprintf(buf, sizeof buf, "a device-side barrier timed out (reason %llu): fail-stop", reason);
+    }
+    broken_msg = buf;
+    fail(BL_ERR_NCCL, buf);
+  }
+  if (e[kErrGrad] != none) {  // optimizers.cpp:109-114 (fused check: reported after the step)
     const unsigned long long w = e[kErrGrad] >> 40, k = e[kErrGrad] & ((1ull << 40) - 1);
-    long long layer = -1;
-    if (off) layer = std::upper_bound(off->begin(), off->end(), static_cast<uint64_t>(k)) - off->begin() - 1;
-    std::snprintf(buf, sizeof buf, "non-finite gradient at step %" PRIu64 ", worker %llu, layer 'layer%lld'",
-                  pending_step, w, layer);
+    std::snprintf(buf, sizeof buf, "non-finite gradient at step %" PRIu64 ", worker %llu, layer '%s'",
+                  pending_step, w, layer_label(opt, layer_of(opt, k)).c_str());
+    snaps.clear();
     fail(BL_ERR_RUNTIME, buf);
   }
+  snaps.clear();
   if (e[kErrScale] != none) fail(BL_ERR_INVALID_ARGUMENT, "compress: input vector is not finite");
   if (e[kErrPeer] != none) {
-    std::snprintf(buf, sizeof buf, "fused NVLink exchange: rank %llu never signalled (timeout)",
-                  e[kErrPeer]);
+    std::snprintf(buf, sizeof buf, "fused NVLink exchange: rank %llu never signalled (timeout)", e[kErrPeer]);
     fail(BL_ERR_NCCL, buf);
   }
   if (e[kErrVerify] != none) {  // comm_sim.cpp:91-101
@@ -675,15 +832,15 @@ void bl_cluster::check_errors(const std::vector<uint64_t>* off) {
     fail(BL_ERR_LOGIC, buf);
   }
   if (e[kErrRecon] != none) {  // optimizers.cpp:288-293
-    std::snprintf(buf, sizeof buf, "non-finite reconstructed gradient for layer 'layer%llu'",
-                  e[kErrRecon]);
+    std::snprintf(buf, sizeof buf, "non-finite reconstructed gradient for layer '%s'",
+                  layer_label(opt, static_cast<long long>(e[kErrRecon])).c_str());
     fail(BL_ERR_RUNTIME, buf);
   }
 }
 
-void bl_cluster::sync_and_check(const std::vector<uint64_t>* off) {
+void bl_cluster::sync_and_check(const bl_optimizer* opt) {
   cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
-  check_errors(off);
+  check_errors(opt);
 }
 
 // ---------------------------------------------------------------------------
@@ -704,6 +861,7 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   if (!single) cl->lossless(true);
   cl->ledger_lossless();
   W1Params w1{};
+  w1.gate = cl->err;
   w1.lt = lt();
   w1.gbar = single ? cl->in : cl->out;
   w1.m = m;
@@ -723,6 +881,7 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   cl->end(KC_W1, a, launch_w1(w1, cl->grid(tiles), cl->stream));
 
   WEpiParams we{};
+  we.gate = cl->err;
   we.L = L;
   we.layer_tile_start = layer_tile_start;
   we.off = off_dev;
@@ -752,6 +911,7 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   cl->end(KC_WEPI, a, launch_wepilogue(we, cl->stream));
 
   W2Params w2{};
+  w2.gate = cl->err;
   w2.lt = lt();
   w2.m = m;
   w2.v = v;
@@ -765,7 +925,7 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   cl->end(KC_W2, a, launch_w2(w2, cl->grid(tiles), cl->stream));
 }
 
-void bl_optimizer::compressed_step(double lr) {
+void bl_optimizer::compressed_step(double lr, const float* stage_host) {
   const bool identity = cl->cfg.compressor != BL_COMPRESSOR_ONEBIT;
   // optimizers.cpp:271-303: ratio rule (onebit_lamb), c = c_avg (basic), c = 1 (adam)
   const int emode = variant == BL_ONEBIT_LAMB ? 0 : variant == BL_LAMB_BASIC_ONEBIT ? 1 : 2;
@@ -801,6 +961,7 @@ void bl_optimizer::compressed_step(double lr) {
     p.n_slow = k1_n_slow;
     p.order = k1_order;
     cl->verify_es_one = !hp.scaled_error_feedback;
+    cl->stage_host = stage_host;  // consumed (and cleared) by compressed() itself
     cl->compressed(&p, mode, 1.0f, es);
   }
 
@@ -835,6 +996,7 @@ void bl_optimizer::compressed_step(double lr) {
   cl->end(KC_K5, a, launch_k5(k5, cl->grid(tiles), cl->stream));
 
   EpiParams ep{};
+  ep.gate = cl->err;
   ep.L = L;
   ep.layer_tile_start = layer_tile_start;
   ep.tile_max = tile_max;
@@ -857,6 +1019,7 @@ void bl_optimizer::compressed_step(double lr) {
   cl->end(KC_EPI, a, launch_epilogue(ep, cl->stream));
 
   K6Params k6{};
+  k6.gate = cl->err;
   k6.lt = lt();
   k6.n = cl->n;
   k6.c = cl->c;
@@ -888,8 +1051,11 @@ void bl_optimizer::step(const float* const* grads, int n_grads, uint64_t t, doub
   const bool two = two_stage();
   const bool adam = variant == BL_ADAM || variant == BL_ONEBIT_ADAM;
   bool compressed = false;
+  cl->ensure_usable();
+  cl->last_opt = this;
   if (!two || t < hp.warmup_steps) {
     cl->copy_inputs(grads, n_grads, d, memory);
+    cl->begin_step(this, t, true, strict);  // strict: check_gradients before any mutation
     const bool finalize = two && t + 1 == hp.warmup_steps;
     warmup_step(t, lr, two && !adam, finalize, adam);
     if (finalize) {  // optimizers.cpp:202-224
@@ -908,13 +1074,15 @@ void bl_optimizer::step(const float* const* grads, int n_grads, uint64_t t, doub
     // into tile-aligned pieces and K1 starts on each piece as it lands
     // (bl_cluster::compressed).  BL_OVERLAP_H2D=0 copies first.
     const char* ov = std::getenv("BL_OVERLAP_H2D");
-    if (memory == BL_MEM_HOST && cl->nw == 1 && cl->cfg.compressor == BL_COMPRESSOR_ONEBIT &&
+    const float* stage = nullptr;
+    if (memory == BL_MEM_HOST && cl->nw == 1 && cl->cfg.compressor == BL_COMPRESSOR_ONEBIT && !strict &&
         !(ov && ov[0] == '0')) {
-      cl->stage_host = grads[0];
+      stage = grads[0];  // strict mode checks the whole gradient first: no piecewise copy
     } else {
       cl->copy_inputs(grads, n_grads, d, memory);
     }
-    compressed_step(lr);
+    cl->begin_step(this, t, true, strict);
+    compressed_step(lr, stage);
     compressed = true;
   }
   cl->pending_step = t;
@@ -927,7 +1095,7 @@ void bl_optimizer::step(const float* const* grads, int n_grads, uint64_t t, doub
                                cl->stream),
                "trace copy");
     cl->end(KC_D2H, a, 0);
-    cl->sync_and_check(&off);
+    cl->sync_and_check(this);
     for (int l = 0; l < L; ++l) {
       if (tr->c) tr->c[l] = h[l];
       if (tr->r) tr->r[l] = h[L + l];
@@ -977,6 +1145,84 @@ void size_check(uint64_t a, uint64_t b, const char* what) {  // errors.hpp:43-48
     fail(BL_ERR_DIMENSION, std::string(what) + ": size mismatch (" + std::to_string(a) + " vs " +
                                std::to_string(b) + ")");
   }
+}
+
+}  // namespace
+
+// ---- free functions ---------------------------------------------------------
+namespace {
+
+// Device allocations of one synchronous free-function call.
+struct Scratch {
+  std::vector<void*> ptrs;
+  ~Scratch() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  T* get(size_t n) {
+    T* p = dalloc<T>(n);
+    ptrs.push_back(p);
+    return p;
+  }
+};
+
+// FusedLayout (fusion.cpp:26-36) + layer tile tables on the device.
+struct DevLayout {
+  uint64_t d = 0;
+  int L = 0, tiles = 0;
+  uint64_t* off = nullptr;
+  int* tile_layer = nullptr;
+  int* tile_start = nullptr;
+  DevLayout(const uint64_t* sizes, int n_layers, Scratch& s) : L(n_layers) {
+    std::vector<uint64_t> o(static_cast<size_t>(L) + 1, 0);
+    std::vector<int> ts(static_cast<size_t>(L) + 1, 0);
+    for (int l = 0; l < L; ++l) {
+      o[l + 1] = o[l] + sizes[l];
+      ts[l + 1] = ts[l] + static_cast<int>((sizes[l] + kTile - 1) / kTile);
+    }
+    d = o[L];
+    tiles = ts[L];
+    std::vector<int> tl(static_cast<size_t>(std::max(tiles, 1)), 0);
+    for (int l = 0; l < L; ++l)
+      for (int t = ts[l]; t < ts[l + 1]; ++t) tl[t] = l;
+    off = reinterpret_cast<uint64_t*>(s.get<double>(o.size()));
+    tile_start = reinterpret_cast<int*>(s.get<float>(ts.size()));
+    tile_layer = reinterpret_cast<int*>(s.get<float>(tl.size()));
+    cuda_check(cudaMemcpy(off, o.data(), o.size() * 8, cudaMemcpyHostToDevice), "layout");
+    cuda_check(cudaMemcpy(tile_start, ts.data(), ts.size() * 4, cudaMemcpyHostToDevice), "layout");
+    cuda_check(cudaMemcpy(tile_layer, tl.data(), tl.size() * 4, cudaMemcpyHostToDevice), "layout");
+  }
+};
+
+int check_device(int32_t device) {
+  int ndev = 0;
+  cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (ndev == 0) fail(BL_ERR_CUDA, "no CUDA device");
+  check_arg(device >= 0 && device < ndev, "device ordinal out of range");
+  return device;
+}
+
+void scale_layers(float* fused, const uint64_t* sizes, int32_t n_layers, const double* coeff, int32_t memory,
+                  int32_t device, bool remove) {
+  check_arg(n_layers >= 1, remove ? "remove_scaling: no layers" : "apply_scaling: no layers");
+  DeviceGuard g(check_device(device));
+  Scratch s;
+  DevLayout lay(sizes, n_layers, s);
+  std::vector<float> mul(static_cast<size_t>(n_layers));
+  for (int l = 0; l < n_layers; ++l)  // kernels::scale(view, c) / (view, 1.0 / c), fusion.cpp:130-145
+    mul[l] = static_cast<float>(remove ? 1.0 / coeff[l] : coeff[l]);
+  float* dmul = s.get<float>(mul.size());
+  cuda_check(cudaMemcpy(dmul, mul.data(), mul.size() * 4, cudaMemcpyHostToDevice), "scales");
+  float* x = fused;
+  if (memory == BL_MEM_HOST) {
+    x = s.get<float>(lay.d);
+    cuda_check(cudaMemcpy(x, fused, lay.d * 4, cudaMemcpyHostToDevice), "fused in");
+  }
+  launch_scale_layers(x, lay.off, n_layers, dmul, lay.d, nullptr);
+  cuda_check(cudaGetLastError(), "scale kernel");
+  if (memory == BL_MEM_HOST)
+    cuda_check(cudaMemcpy(fused, x, lay.d * 4, cudaMemcpyDeviceToHost), "fused out");
+  cuda_check(cudaDeviceSynchronize(), "scaling");
 }
 
 }  // namespace
@@ -1065,9 +1311,10 @@ bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
       c->wpart = dalloc<double>(nw * n * c->tpc);
       c->spart = dalloc<double>(static_cast<size_t>(c->ns) * c->tpc);
       c->out = dalloc<float>(c->P + kSlack);
-      c->err = reinterpret_cast<unsigned long long*>(dalloc<double>(kErrSlots));
+      c->err = reinterpret_cast<unsigned long long*>(dalloc<double>(kErrWords));
       c->tile_ctr = reinterpret_cast<unsigned int*>(dalloc<float>(4));
       cuda_check(cudaMemset(c->err, 0xFF, kErrSlots * sizeof(unsigned long long)), "err init");
+      c->set_peer_timeout(c->peer_timeout_ms);
       if (cfg->endpoint_stats) {
         c->wcmax = dalloc<float>(nw * n * c->tpc);
         c->scmax = dalloc<float>(static_cast<size_t>(c->ns) * c->tpc);
@@ -1114,6 +1361,7 @@ void bl_cluster_destroy(bl_cluster* c) {
   if (!c) return;
   DeviceGuard g(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (bl_optimizer* o : c->opts) o->cl = nullptr;  // orphaned: their destroy only frees memory
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (c->comm) ncclCommDestroy(c->comm);
   void* bufs[] = {c->in,        c->werr,       c->wpk[0],          c->wpk[1],    c->rpk,
@@ -1140,6 +1388,27 @@ void bl_cluster_destroy(bl_cluster* c) {
 int32_t bl_cluster_transport(const bl_cluster* c) { return c ? c->transport : BL_TRANSPORT_NCCL; }
 void* bl_cluster_stream(const bl_cluster* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
+bl_status bl_cluster_get_config(const bl_cluster* c, bl_cluster_config* outp) {
+  return guarded([&] {
+    *outp = c->cfg;
+    outp->transport = c->mode == BL_MODE_NCCL ? c->transport : c->cfg.transport;
+    outp->stream = c->stream;
+  });
+}
+
+uint64_t bl_cluster_step_count(const bl_cluster* c) {
+  return c ? c->ledger.compressed_collectives + c->ledger.lossless_collectives : 0;
+}
+
+bl_status bl_cluster_set_peer_timeout(bl_cluster* c, double ms) {
+  return guarded([&] {
+    check_arg(ms > 0.0, "peer timeout must be > 0 ms");
+    DeviceGuard g(c->device);
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    c->set_peer_timeout(ms);
+  });
+}
+
 bl_status bl_cluster_dims(const bl_cluster* c, uint64_t* padded, uint64_t* chunk) {
   return guarded([&] {
     if (padded) *padded = c->P;
@@ -1155,7 +1424,9 @@ bl_status bl_cluster_compressed_allreduce(bl_cluster* c, const float* const* inp
     size_check(static_cast<uint64_t>(n_inputs), static_cast<uint64_t>(c->nw),
                "compressed_allreduce: worker count");
     size_check(len, c->dim, "compressed_allreduce: input length");
+    c->ensure_usable();
     c->copy_inputs(inputs, n_inputs, len, memory);
+    c->begin_step(nullptr, 0, false, false);
     if (c->cfg.compressor == BL_COMPRESSOR_IDENTITY) {
       // Identity compressor: lossless messages, residuals stay zero
       // (compression.cpp:184-188), result = ascending-worker average.
@@ -1170,7 +1441,7 @@ bl_status bl_cluster_compressed_allreduce(bl_cluster* c, const float* const* inp
         cudaEvent_t a;
         c->begin(KC_DEC, &a);
         c->end(KC_DEC, a, launch_decompress(c->res[latest], c->n, c->c, c->slot, c->W, c->dim, c->out,
-                                            c->stream));
+                                            c->err, c->stream));
       }
     }
     c->pending_is_step = false;
@@ -1189,7 +1460,9 @@ bl_status bl_cluster_lossless_allreduce(bl_cluster* c, const float* const* input
     size_check(static_cast<uint64_t>(n_inputs), static_cast<uint64_t>(c->nw),
                "lossless_allreduce: worker count");
     size_check(len, c->dim, "lossless_allreduce: input length");
+    c->ensure_usable();
     c->copy_inputs(inputs, n_inputs, len, memory);
+    c->begin_step(nullptr, 0, false, false);
     c->lossless(false);
     c->ledger_lossless();
     if (outp) {
@@ -1373,8 +1646,9 @@ static void validate(const bl_hparams* h) {
   if (h->warmup_steps > h->total_steps) reject("warmup_steps must not exceed total_steps");
 }
 
-bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_layers,
-                              const bl_hparams* hp, bl_cluster* cl, bl_optimizer** out) {
+static bl_status optimizer_create(int32_t variant, const uint64_t* sizes, const char* const* names,
+                                  int32_t n_layers, const bl_hparams* hp, bl_cluster* cl,
+                                  bl_optimizer** out) {
   return guarded([&] {
     *out = nullptr;
     validate(hp);
@@ -1389,6 +1663,9 @@ bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_
       o->L = n_layers;
       o->hp = *hp;
       o->cl = cl;
+      o->names.resize(static_cast<size_t>(n_layers));
+      for (int l = 0; l < n_layers; ++l)
+        o->names[l] = names && names[l] ? std::string(names[l]) : "layer" + std::to_string(l);
       o->off.assign(static_cast<size_t>(n_layers) + 1, 0);
       std::vector<int> tstart(static_cast<size_t>(n_layers) + 1, 0);
       for (int l = 0; l < n_layers; ++l) {
@@ -1489,14 +1766,46 @@ bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_
       bl_optimizer_destroy(o);
       throw;
     }
+    cl->opts.push_back(o);
     *out = o;
   });
 }
 
+bl_status bl_optimizer_create(int32_t variant, const uint64_t* sizes, int32_t n_layers,
+                              const bl_hparams* hp, bl_cluster* cl, bl_optimizer** out) {
+  return optimizer_create(variant, sizes, nullptr, n_layers, hp, cl, out);
+}
+
+bl_status bl_optimizer_create_named(int32_t variant, const bl_layer_spec* layers, int32_t n_layers,
+                                    const bl_hparams* hp, bl_cluster* cl, bl_optimizer** out) {
+  std::vector<uint64_t> sizes(static_cast<size_t>(std::max(n_layers, 0)));
+  std::vector<const char*> names(sizes.size());
+  for (size_t l = 0; l < sizes.size(); ++l) {
+    sizes[l] = layers[l].size;
+    names[l] = layers[l].name;
+  }
+  return optimizer_create(variant, sizes.data(), names.data(), n_layers, hp, cl, out);
+}
+
+const char* bl_optimizer_layer_name(const bl_optimizer* o, int32_t layer) {
+  if (!o || layer < 0 || layer >= o->L) return nullptr;
+  return o->names[static_cast<size_t>(layer)].c_str();
+}
+
+bl_status bl_optimizer_set_strict(bl_optimizer* o, int32_t on) {
+  return guarded([&] { o->strict = on != 0; });
+}
+
 void bl_optimizer_destroy(bl_optimizer* o) {
   if (!o) return;
-  DeviceGuard g(o->cl->device);
-  cudaStreamSynchronize(o->cl->stream);
+  if (bl_cluster* c = o->cl) {  // null when the cluster was destroyed first
+    DeviceGuard g(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->last_opt == o) c->last_opt = nullptr;
+    for (auto& sn : c->snaps)
+      if (sn.opt == o) sn.opt = nullptr;
+    c->opts.erase(std::remove(c->opts.begin(), c->opts.end(), o), c->opts.end());
+  }
   void* bufs[] = {o->off_dev, o->tile_layer, o->layer_tile_start, o->x, o->m, o->v, o->vf,
                   o->mprev, o->c_avg, o->r_prev, o->coeff, o->mag, o->A, o->B, o->invc, o->coef_x,
                   o->trace, o->cmean, o->es, o->counter, o->tile_sums, o->tile_max,
@@ -1510,6 +1819,7 @@ bl_status bl_optimizer_step(bl_optimizer* o, bl_cluster* c, const float* const* 
                             int32_t n_grads, uint64_t t, double lr, int32_t memory,
                             bl_step_trace* trace) {
   return guarded([&] {
+    if (!o->cl) fail(BL_ERR_LOGIC, "step: the optimizer's cluster was destroyed");
     if (c != o->cl) fail(BL_ERR_LOGIC, "step: optimizer is bound to a different cluster");
     DeviceGuard g(c->device);
     o->step(grads, n_grads, t, lr, memory, trace);
@@ -1522,8 +1832,9 @@ float* bl_optimizer_grad_buffer(bl_optimizer* o, int32_t worker) {
 
 bl_status bl_optimizer_get_state(bl_optimizer* o, int32_t which, float* host_out) {
   return guarded([&] {
+    if (!o->cl) fail(BL_ERR_LOGIC, "the optimizer's cluster was destroyed");
     DeviceGuard g(o->cl->device);
-    o->cl->sync_and_check(&o->off);
+    o->cl->sync_and_check(o);
     const float* src = nullptr;
     switch (which) {
       case BL_STATE_X: src = o->x; break;
@@ -1561,8 +1872,9 @@ bl_status bl_optimizer_get_state(bl_optimizer* o, int32_t which, float* host_out
 
 bl_status bl_optimizer_set_state(bl_optimizer* o, int32_t which, const float* host_in) {
   return guarded([&] {
+    if (!o->cl) fail(BL_ERR_LOGIC, "the optimizer's cluster was destroyed");
     DeviceGuard g(o->cl->device);
-    o->cl->sync_and_check(&o->off);
+    o->cl->sync_and_check(o);
     float* dst = nullptr;
     switch (which) {
       case BL_STATE_X: dst = o->x; break;
@@ -1602,8 +1914,9 @@ bl_status bl_optimizer_set_state(bl_optimizer* o, int32_t which, const float* ho
 
 bl_status bl_optimizer_get_scalars(bl_optimizer* o, double* c_avg, double* r_prev, double* coeff) {
   return guarded([&] {
+    if (!o->cl) fail(BL_ERR_LOGIC, "the optimizer's cluster was destroyed");
     DeviceGuard g(o->cl->device);
-    o->cl->sync_and_check(&o->off);
+    o->cl->sync_and_check(o);
     const size_t L = static_cast<size_t>(o->L);
     if (c_avg) cuda_check(cudaMemcpy(c_avg, o->c_avg, L * 8, cudaMemcpyDeviceToHost), "c_avg");
     if (r_prev) cuda_check(cudaMemcpy(r_prev, o->r_prev, L * 8, cudaMemcpyDeviceToHost), "r_prev");
@@ -1613,8 +1926,9 @@ bl_status bl_optimizer_get_scalars(bl_optimizer* o, double* c_avg, double* r_pre
 
 bl_status bl_optimizer_set_scalars(bl_optimizer* o, const double* c_avg, const double* r_prev) {
   return guarded([&] {
+    if (!o->cl) fail(BL_ERR_LOGIC, "the optimizer's cluster was destroyed");
     DeviceGuard g(o->cl->device);
-    o->cl->sync_and_check(&o->off);
+    o->cl->sync_and_check(o);
     const size_t L = static_cast<size_t>(o->L);
     if (c_avg) cuda_check(cudaMemcpy(o->c_avg, c_avg, L * 8, cudaMemcpyHostToDevice), "c_avg");
     if (r_prev) cuda_check(cudaMemcpy(o->r_prev, r_prev, L * 8, cudaMemcpyHostToDevice), "r_prev");
@@ -1624,5 +1938,114 @@ bl_status bl_optimizer_set_scalars(bl_optimizer* o, const double* c_avg, const d
 int32_t bl_optimizer_frozen(const bl_optimizer* o) { return o && o->frozen ? 1 : 0; }
 uint64_t bl_optimizer_fused_dim(const bl_optimizer* o) { return o ? o->d : 0; }
 int32_t bl_optimizer_layer_count(const bl_optimizer* o) { return o ? o->L : 0; }
+
+
+bl_status bl_compute_scales(const float* m, const uint64_t* sizes, int32_t n_layers, double floor_,
+                            double* coeff_out, double* reference_out, int32_t memory, int32_t device) {
+  return guarded([&] {
+    check_arg(n_layers >= 1, "compute_scales: no layers");  // fusion.cpp:109-110
+    check_arg(floor_ > 0.0, "compute_scales: floor must be positive");
+    DeviceGuard g(check_device(device));
+    Scratch s;
+    DevLayout lay(sizes, n_layers, s);
+    const float* x = m;
+    if (memory == BL_MEM_HOST) {
+      float* t = s.get<float>(lay.d);
+      cuda_check(cudaMemcpy(t, m, lay.d * 4, cudaMemcpyHostToDevice), "momentum in");
+      x = t;
+    }
+    double* part = s.get<double>(static_cast<size_t>(std::max(lay.tiles, 1)));
+    double* mag = s.get<double>(static_cast<size_t>(n_layers));
+    double* coeff = s.get<double>(static_cast<size_t>(n_layers));
+    double* ref = s.get<double>(1);
+    unsigned int* counter = reinterpret_cast<unsigned int*>(s.get<float>(1));
+    if (lay.tiles > 0) launch_layer_abs_tiles(x, lay.off, lay.tile_layer, lay.tile_start, lay.tiles, part, nullptr);
+    launch_scales_final(n_layers, lay.tile_start, lay.off, part, floor_, mag, coeff, ref, counter, nullptr);
+    cuda_check(cudaGetLastError(), "compute_scales kernels");
+    if (coeff_out)
+      cuda_check(cudaMemcpy(coeff_out, coeff, static_cast<size_t>(n_layers) * 8, cudaMemcpyDeviceToHost),
+                 "coeff");
+    if (reference_out) cuda_check(cudaMemcpy(reference_out, ref, 8, cudaMemcpyDeviceToHost), "reference");
+    cuda_check(cudaDeviceSynchronize(), "compute_scales");
+  });
+}
+
+bl_status bl_apply_scaling(float* fused, const uint64_t* sizes, int32_t n_layers, const double* coeff,
+                           int32_t memory, int32_t device) {
+  return guarded([&] { scale_layers(fused, sizes, n_layers, coeff, memory, device, false); });
+}
+
+bl_status bl_remove_scaling(float* fused, const uint64_t* sizes, int32_t n_layers, const double* coeff,
+                            int32_t memory, int32_t device) {
+  return guarded([&] { scale_layers(fused, sizes, n_layers, coeff, memory, device, true); });
+}
+
+bl_status bl_compress_with_feedback(const float* v, float* delta, uint64_t len, int32_t compressor,
+                                    double error_scale, uint8_t* wire, float* dec, int32_t memory,
+                                    int32_t device) {
+  return guarded([&] {
+    check_arg(compressor == BL_COMPRESSOR_ONEBIT || compressor == BL_COMPRESSOR_IDENTITY,
+              "compress_with_feedback: unknown compressor");
+    check_device(device);
+    if (len == 0) {  // empty block: no sign bytes, scale 0 (compression.cpp:54)
+      if (wire && compressor == BL_COMPRESSOR_ONEBIT) std::memset(wire, 0, 4);
+      return;
+    }
+    // One endpoint of a one-worker cluster is exactly this function: its
+    // residual slot holds delta (deferred form with a zero previous scale,
+    // so delta = raw - (+-0) = raw), K1 compresses v + es*delta.
+    bl_cluster_config cfg{};
+    cfg.n_workers = 1;
+    cfg.mode = BL_MODE_SIM;
+    cfg.device = device;
+    cfg.dim = len;
+    cfg.compressor = BL_COMPRESSOR_ONEBIT;
+    cfg.baseline_bits_per_element = 16;
+    cfg.compensation_tolerance = 1e-12;
+    bl_cluster* cp = nullptr;
+    if (bl_cluster_create(&cfg, &cp) != BL_OK) fail(BL_ERR_CUDA, g_err);
+    std::unique_ptr<bl_cluster, void (*)(bl_cluster*)> own(cp, bl_cluster_destroy);
+    bl_cluster* c = cp;
+    DeviceGuard g(device);
+    const size_t bytes = len * sizeof(float);
+    cuda_check(cudaMemcpy(c->werr, delta, bytes, cudaMemcpyDefault), "delta in");
+    if (compressor == BL_COMPRESSOR_IDENTITY) {
+      // corrected = 1*v + es*delta (compression.cpp:181) is the message; delta = 0 (:184-188)
+      std::vector<uint64_t> off = {0, len};
+      const float ab[2] = {1.0f, static_cast<float>(error_scale)};
+      Scratch s;
+      uint64_t* doff = reinterpret_cast<uint64_t*>(s.get<double>(2));
+      float* dab = s.get<float>(2);
+      cuda_check(cudaMemcpy(doff, off.data(), 16, cudaMemcpyHostToDevice), "off");
+      cuda_check(cudaMemcpy(dab, ab, 8, cudaMemcpyHostToDevice), "ab");
+      // in = A*m + B*in with m = v, in = delta: 1*v + es*delta
+      cuda_check(cudaMemcpy(c->in, delta, bytes, cudaMemcpyDefault), "delta in");
+      float* vd = s.get<float>(len);
+      cuda_check(cudaMemcpy(vd, v, bytes, cudaMemcpyDefault), "v in");
+      launch_build_stream(c->in, c->in_stride, 1, len, vd, doff, 1, dab, dab + 1, nullptr, 0, c->stream);
+      cuda_check(cudaStreamSynchronize(c->stream), "identity");
+      if (dec) cuda_check(cudaMemcpy(dec, c->in, bytes, cudaMemcpyDefault), "decompressed out");
+      cuda_check(memory == BL_MEM_HOST ? (std::memset(delta, 0, bytes), cudaSuccess) : cudaMemset(delta, 0, bytes),
+                 "delta reset");
+      return;
+    }
+    cuda_check(cudaMemcpy(c->in, v, bytes, cudaMemcpyDefault), "v in");
+    c->compressed(nullptr, 0, static_cast<float>(error_scale), nullptr, nullptr);
+    cuda_check(cudaStreamSynchronize(c->stream), "compress");
+    unsigned long long e[kErrSlots];
+    cuda_check(cudaMemcpy(e, c->err, sizeof e, cudaMemcpyDeviceToHost), "error words");
+    if (e[kErrScale] < (1ull << 20))  // the worker endpoint (key 0; the server's is 1 << 20)
+      fail(BL_ERR_INVALID_ARGUMENT, "compress: input vector is not finite");  // :56-58, delta untouched
+    const int latest = static_cast<int>((c->calls + 1u) & 1u);
+    if (wire) packet_bytes(c, c->wpk[latest], wire);
+    if (dec) {
+      launch_decompress(c->wpk[latest], 1, c->c, c->slot, c->W, len, c->out, c->err, c->stream);
+      cuda_check(cudaMemcpyAsync(dec, c->out, bytes, cudaMemcpyDefault, c->stream), "decompressed out");
+    }
+    launch_materialize_error(c->werr, c->c_pad, c->wpk[latest], c->slot, c->W, c->c, len, c->out, c->stream);
+    cuda_check(cudaMemcpyAsync(delta, c->out, bytes, cudaMemcpyDefault, c->stream), "delta out");
+    cuda_check(cudaStreamSynchronize(c->stream), "compress outputs");
+  });
+}
 
 }  // extern "C"

@@ -43,7 +43,7 @@ class DeviceGuard {
 // Kernel classes for launch counting and optional CUDA-event timing.
 enum KClass : int {
   KC_K1 = 0, KC_FIN, KC_K3, KC_K5, KC_EPI, KC_K6, KC_W1, KC_WEPI, KC_W2, KC_AVG,
-  KC_DEC, KC_MAT, KC_STATS, KC_A2A, KC_AG, KC_H2D, KC_D2H, KC_K1B, KC_SMALL, KC_COUNT
+  KC_DEC, KC_MAT, KC_STATS, KC_A2A, KC_AG, KC_H2D, KC_D2H, KC_K1B, KC_SMALL, KC_GATE, KC_COUNT
 };
 extern const char* const kClassNames[KC_COUNT];
 
@@ -54,6 +54,8 @@ T* dalloc(size_t n);  // zero-initialised device allocation
 int* boundary_first_order(const std::vector<int>& slow, int reps, int per);
 
 }  // namespace bl
+
+struct bl_optimizer;
 
 struct bl_cluster {
   bl_cluster_config cfg{};
@@ -98,6 +100,11 @@ struct bl_cluster {
   unsigned int* lossless_done = nullptr;
   unsigned int* small_bar = nullptr;  // grid barrier of the fused small collective
   unsigned long long lcalls = 0;      // lossless collectives run (flag epoch)
+  // Step gate (bl_kernels.cuh GateParams): arrival words at flags[4n + q],
+  // rank 0's decision word at flags[5n].
+  unsigned long long gate_epoch = 0;
+  unsigned long long* gate_status = nullptr;  // NCCL transport: min-reduced status word
+  double peer_timeout_ms = 600000.0;          // fail-stop bound of every peer wait
   std::vector<void*> ipc_opened;
   void setup_p2p(bool required);
 
@@ -134,6 +141,33 @@ struct bl_cluster {
   uint64_t pending_step = 0;    // step index of the last asynchronous optimizer step
   bool pending_is_step = false;
 
+  // Transactional steps: the host-side state at the start of every step /
+  // collective not yet confirmed by a clean synchronizing call.  A gate that
+  // closed before any mutation (strict non-finite gradient, late peer) rolls
+  // the host state back to the snapshot of the step it closed at; the device
+  // state is untouched because every later kernel returned at entry.
+  struct Snap {
+    uint64_t seq, t;
+    bool is_step;
+    uint64_t calls, checks;
+    bool last_identity;
+    bl_volume_ledger ledger;
+    bl_optimizer* opt;
+    bool frozen, has_vf, has_mprev, m_valid, mprev_separate;
+    uint64_t my_calls;
+  };
+  std::vector<Snap> snaps;
+  uint64_t seq = 0;
+  bool broken = false;          // fail-stop: a peer died mid-step, the state is undefined
+  std::string broken_msg;
+  // Start of a step / collective: snapshot, then the strict pre-pass and the
+  // gate (arrival barrier when multi-process).  `opt` may be null.
+  void begin_step(bl_optimizer* opt, uint64_t t, bool is_step, bool strict);
+  void ensure_usable() const;
+  void set_peer_timeout(double ms);
+  bl_optimizer* last_opt = nullptr;  // optimizer of the latest step (layer names in messages)
+  std::vector<bl_optimizer*> opts;   // live optimizers bound to this cluster
+
   int cur() const { return static_cast<int>(calls & 1u); }
   int prev() const { return static_cast<int>((calls + 1u) & 1u); }
 
@@ -153,8 +187,9 @@ struct bl_cluster {
   void finish_compressed(float es_host, const float* es_dev);
   void lossless(bool check_finite);  // in -> out (averaged), ledger
   void refresh_stats();
-  void check_errors(const std::vector<uint64_t>* layer_off);
-  void sync_and_check(const std::vector<uint64_t>* layer_off);
+  void check_errors(const bl_optimizer* opt);
+  void sync_and_check(const bl_optimizer* opt);
+  void rollback(uint64_t seq_closed);
   void ledger_compressed();
   void ledger_lossless();
   uint64_t chunk_payload_bits(uint64_t j) const;
@@ -186,6 +221,8 @@ struct bl_optimizer {
   int k1_n_slow = 0;
   int* k1_order = nullptr;       // K1 processing order, boundary tiles first
   bool frozen = false, has_vf = false, has_mprev = false;
+  std::vector<std::string> names;  // layer names (LayerSpec::name) for error messages
+  bool strict = false;          // read-only finite pre-pass before any mutation (optimizers.cpp:99-117)
   bool m_valid = true;          // m buffer holds m (else: decompressed result * invc)
   bool mprev_separate = false;  // m_prev poked by the caller
   uint64_t my_calls = 0;        // cluster->calls after our last compressed step
@@ -197,6 +234,6 @@ struct bl_optimizer {
   void step(const float* const* grads, int n_grads, uint64_t t, double lr, int memory,
             bl_step_trace* trace_out);
   void warmup_step(uint64_t t, double lr, bool track, bool finalize, bool adam);
-  void compressed_step(double lr);
+  void compressed_step(double lr, const float* stage_host);
   void materialize_m(float* dst);
 };

@@ -124,6 +124,12 @@ def main() -> int:
     for tp in transports:
         optimizer_check(rank, world, local, new_uid, check, tp)
 
+    # ---- 3. strict mode and fail-stop (transactional steps) ----------------
+    for tp in transports:
+        strict_check(rank, world, local, new_uid, check, tp)
+    if "p2p" in transports:
+        failstop_check(rank, world, local, new_uid, check, "p2p")
+
     ok = torch.tensor([0 if failures else 1], device="cuda")
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     if rank == 0:
@@ -176,7 +182,8 @@ def optimizer_check(rank, world, local, new_uid, check, tp):
 
     # check_gradients (optimizers.cpp:99-117) in the multi-process warmup: a
     # non-finite element of the last rank's gradient lying in chunk 0 is read
-    # by rank 0 (over NVLink in P2P mode) and reported to its owner only.
+    # by rank 0 (over NVLink in P2P mode) and forwarded to every rank, so every
+    # rank raises the reference's message (fused mode: after the step).
     cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid(),
                        transport=tp)
     opt = bl.Optimizer("onebit_lamb", sizes, hp, cl)
@@ -190,11 +197,127 @@ def optimizer_check(rank, world, local, new_uid, check, tp):
             raised = ""
         except Exception as exc:  # noqa: BLE001 - the message is checked below
             raised = str(exc)
-        if bad:
+        if bad or (t == 2 and tp == "p2p"):
             check("non-finite gradient" in raised and f"worker {world - 1}" in raised,
-                  f"{tp} non-finite gradient reported to its owner: {raised!r}")
-        else:
+                  f"{tp} rank {rank}: non-finite gradient not reported: {raised!r}")
+        elif t < 2:
             check(raised == "", f"{tp} rank {rank} t={t} unexpected error {raised!r}")
+    opt.close()
+    cl.close()
+
+
+def state_bytes(opt, cl, rank):
+    return b"".join(opt.get(k).tobytes() for k in ("x", "m", "v", "v_frozen")) + \
+        cl.worker_error(rank).tobytes() + cl.server_error(rank).tobytes() + cl.server_packet(rank)
+
+
+def strict_check(rank, world, local, new_uid, check, tp):
+    """Strict mode (optimizers.cpp:99-117,337): a non-finite element in the
+    last rank's gradient, in the warmup stage and in the compression stage,
+    raises the reference's message on EVERY rank before anything changed; the
+    run then continues bit-identically to a simulated cluster that never saw
+    the bad steps."""
+    sizes = [3000, 2, 1024, 1023, 5000, 3, 4096 * 3 + 17, 77777]
+    names = [f"layer.{i}" for i in range(len(sizes))]
+    layout = list(zip(names, sizes))
+    d = sum(sizes)
+    steps, warm = 10, 4
+    hp = bl.HyperParams(total_steps=steps + 2, warmup_steps=warm)
+    cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid(), transport=tp)
+    opt = bl.Optimizer("onebit_lamb", layout, hp, cl, strict=True)
+    if rank == 0:
+        sim = bl.SimCluster(world, d, device=local)
+        sopt = bl.Optimizer("onebit_lamb", layout, hp, sim, strict=True)
+    rng = np.random.default_rng(17)
+    x0 = (rng.standard_normal(d) * 0.02).astype(np.float32)
+    opt.set("x", x0)
+    if rank == 0:
+        sopt.set("x", x0)
+    sig = np.repeat(10.0 ** (-4 + 2 * rng.random(len(sizes))), sizes).astype(np.float32)
+    t = 0
+    while t < steps:
+        g = (rng.standard_normal((world, d)) * sig).astype(np.float32)
+        for bad_t in (2, 6):  # one warmup-stage and one compression-stage rejection
+            if t == bad_t:
+                gb = g.copy()
+                gb[world - 1, 3000 + 2 + 1024 + 17] = np.inf  # layer.3
+                before = state_bytes(opt, cl, rank)
+                try:
+                    opt.step(gb[rank:rank + 1], t, 1e-3)
+                    raised = ""
+                except bl.NumericalError as exc:
+                    raised = str(exc)
+                want = f"non-finite gradient at step {t}, worker {world - 1}, layer 'layer.3'"
+                check(raised == want, f"{tp} strict rank {rank} t={t}: {raised!r} != {want!r}")
+                check(state_bytes(opt, cl, rank) == before, f"{tp} strict rank {rank} t={t}: state changed")
+                if rank == 0:
+                    try:
+                        sopt.step(gb, t, 1e-3)
+                        sraised = ""
+                    except bl.NumericalError as exc:
+                        sraised = str(exc)
+                    check(sraised == want, f"sim strict t={t}: {sraised!r}")
+        tr = opt.step(g[rank:rank + 1], t, 1e-3)
+        xs = gather_bytes(opt.get("x").tobytes() + tr.c.tobytes())
+        if rank == 0:
+            st = sopt.step(g, t, 1e-3)
+            ref = sopt.get("x").tobytes() + st.c.tobytes()
+            for r in range(world):
+                check(xs[r] == ref, f"{tp} strict: x rank {r} t={t} after the rejected steps")
+        t += 1
+    opt.close()
+    cl.close()
+
+
+def failstop_check(rank, world, local, new_uid, check, tp):
+    """A rank late past the peer timeout (host stall before the step) aborts
+    the step on EVERY rank before any state changed -- the late rank included
+    -- instead of letting the others run on stale packets; the next step then
+    proceeds normally and matches a simulated cluster that never saw it."""
+    import time
+
+    sizes = [3000, 2, 1024, 1023, 5000, 3, 4096 * 3 + 17, 77777]
+    d = sum(sizes)
+    hp = bl.HyperParams(total_steps=12, warmup_steps=2)
+    cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid(), transport=tp)
+    cl.set_peer_timeout(1500.0)
+    opt = bl.Optimizer("onebit_lamb", sizes, hp, cl)
+    if rank == 0:
+        sim = bl.SimCluster(world, d, device=local)
+        sopt = bl.Optimizer("onebit_lamb", sizes, hp, sim)
+    rng = np.random.default_rng(23)
+    x0 = (rng.standard_normal(d) * 0.02).astype(np.float32)
+    opt.set("x", x0)
+    if rank == 0:
+        sopt.set("x", x0)
+    sig = np.repeat(10.0 ** (-4 + 2 * rng.random(len(sizes))), sizes).astype(np.float32)
+    for t in range(6):
+        g = (rng.standard_normal((world, d)) * sig).astype(np.float32)
+        for late_t in (1, 4):  # a late rank in the warmup stage and in the compression stage
+            if t != late_t:
+                continue
+            before = state_bytes(opt, cl, rank)
+            if rank == world - 1:
+                time.sleep(4.0)  # > the 1.5 s timeout: the others give up
+            t0 = time.time()
+            try:
+                opt.step(g[rank:rank + 1], t, 1e-3)
+                raised = ""
+            except bl.NcclError as exc:
+                raised = str(exc)
+            took = time.time() - t0
+            check("aborted on every rank before any state changed" in raised,
+                  f"{tp} failstop rank {rank} t={t}: {raised!r}")
+            check(took < 30.0, f"{tp} failstop rank {rank} t={t}: took {took:.1f} s")
+            check(state_bytes(opt, cl, rank) == before, f"{tp} failstop rank {rank} t={t}: state changed")
+            dist.barrier()
+        tr = opt.step(g[rank:rank + 1], t, 1e-3)
+        xs = gather_bytes(opt.get("x").tobytes() + tr.c.tobytes())
+        if rank == 0:
+            st = sopt.step(g, t, 1e-3)
+            ref = sopt.get("x").tobytes() + st.c.tobytes()
+            for r in range(world):
+                check(xs[r] == ref, f"{tp} failstop: x rank {r} t={t}")
     opt.close()
     cl.close()
 
