@@ -327,7 +327,8 @@ __device__ __forceinline__ unsigned long long wait_bound(const unsigned long lon
 // sequence.  The counter resets itself: a launch makes exactly
 // total + nwarps fetches and the last one writes 0 back, which stream order
 // makes visible to the next kernel.
-struct TileSched {
+template <bool SUB = false>
+struct TileSchedT {
   unsigned int* ctr;
   long long total, nwarps, cur;
   const int* order = nullptr;  // dynamic mode: hand out order[v] instead of v
@@ -344,11 +345,18 @@ struct TileSched {
     if (lane == 0) {
       v = atomicAdd(ctr, 1u);
       if (static_cast<long long>(v) == total + nwarps - 1) *ctr = 0u;
-      if (order && static_cast<long long>(v) < total) v = static_cast<unsigned long long>(__ldg(order + v));
+      if (SUB) {  // sub-launch: indices past the end stay past every tile index
+        v = static_cast<long long>(v) < total ? static_cast<unsigned long long>(__ldg(order + v)) : (1ull << 62);
+      } else if (order && static_cast<long long>(v) < total) {
+        v = static_cast<unsigned long long>(__ldg(order + v));
+      }
     }
     return static_cast<long long>(__shfl_sync(0xffffffffu, v, 0));
   }
 };
+using TileSched = TileSchedT<false>;
+// W1/W2 (warmup overlap sub-launches over order[0..count)).
+using TileSchedSub = TileSchedT<true>;
 
 // ---- fused NVLink exchange: epoch flags in peer memory -----------------------
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -1644,7 +1652,7 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0, p.lt.order};  // boundary tiles first
+  TileSchedSub sch{p.lt.ctr, p.lt.count ? p.lt.count : p.lt.tiles, nwarps, 0, p.lt.order};  // boundary first
   for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
@@ -1760,7 +1768,7 @@ __global__ void __launch_bounds__(1024) k_wepilogue(const WEpiParams p) {
   if (gate_closed_call(p.gate)) return;
   __shared__ double shd[32];
   __shared__ bool last;
-  const int l = blockIdx.x;
+  const int l = p.layer_list ? p.layer_list[blockIdx.x] : blockIdx.x;  // sub-launch: a layer subset
   const int t0 = p.layer_tile_start[l], t1 = p.layer_tile_start[l + 1];
   const long long a0 = 4ll * (t0 + threadIdx.x), a1 = 4ll * t1;
   double sx = stripe_sum<4096>(p.tile_sums + 0, a0, a1);
@@ -1838,7 +1846,7 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  TileSched sch{p.lt.ctr, p.lt.tiles, nwarps, 0, p.lt.order};  // boundary tiles first
+  TileSchedSub sch{p.lt.ctr, p.lt.count ? p.lt.count : p.lt.tiles, nwarps, 0, p.lt.order};  // boundary first
   for (long long tile = sch.first(gw, lane); tile < p.lt.tiles; tile = sch.next(lane)) {
     const int l = __ldg(p.lt.tile_layer + tile);
     const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
@@ -2018,6 +2026,13 @@ __device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint
 #ifndef LOSSLESS_U
 #define LOSSLESS_U 2  // 4-float groups per thread per iteration (n = 2, 4)
 #endif
+// Piece p's aligned body of the chunk body [a0, a1): [a0 + off(p), a0 + off(p+1)),
+// off(p) = (p * (a1 - a0) / pieces) rounded down to a multiple of 4 (off(pieces) = a1 - a0).
+__host__ __device__ __forceinline__ uint64_t piece_body_start(uint64_t a0, uint64_t a1, int pieces, int p) {
+  if (p >= pieces) return a1;
+  return a0 + ((static_cast<uint64_t>(p) * (a1 - a0) / static_cast<uint64_t>(pieces)) & ~3ull);
+}
+
 template <int NT>
 __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p) {
   if (gate_closed_call(p.err)) return;
@@ -2030,21 +2045,43 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   constexpr int U = NT == 8 ? 1 : LOSSLESS_U;
-  for (uint64_t k = a0 + 4 * tid; k < a1; k += 4 * nth * U)
-    lossless_groups<NT, U>(p, k, 4 * nth, a1, inv_n);
-  if (blockIdx.x == 0) {  // unaligned head [lo, a0) and tail [a1, hi), one element per thread
-    const uint64_t nh = a0 - lo, nt = hi - a1;
-    if (threadIdx.x < nh + nt) {
-      const uint64_t k = threadIdx.x < nh ? lo + threadIdx.x : a1 + (threadIdx.x - nh);
-      double acc = 0.0;
-      for (int q = 0; q < p.n; ++q) {
-        const float x = __ldcg(p.peer_in[q] + k);
-        if (p.check_finite && !isfinite(x) && k < p.d)
-          flag(p.err, kErrGrad, (static_cast<unsigned long long>(q) << 40) | k);
-        acc += static_cast<double>(x);
+  const int P = p.pieces > 0 ? p.pieces : 1;
+  for (int pc = 0; pc < P; ++pc) {
+    const uint64_t b0 = piece_body_start(a0, a1, P, pc), b1 = piece_body_start(a0, a1, P, pc + 1);
+    for (uint64_t k = b0 + 4 * tid; k < b1; k += 4 * nth * U) lossless_groups<NT, U>(p, k, 4 * nth, b1, inv_n);
+    if (blockIdx.x == 0 && (pc == 0 || pc == P - 1)) {
+      // unaligned head [lo, a0) (first piece) and tail [a1, hi) (last piece), one element per thread
+      const uint64_t nh = pc == 0 ? a0 - lo : 0, nt = pc == P - 1 ? hi - a1 : 0;
+      if (threadIdx.x < nh + nt) {
+        const uint64_t k = threadIdx.x < nh ? lo + threadIdx.x : a1 + (threadIdx.x - nh);
+        double acc = 0.0;
+        for (int q = 0; q < p.n; ++q) {
+          const float x = __ldcg(p.peer_in[q] + k);
+          if (p.check_finite && !isfinite(x) && k < p.d)
+            flag(p.err, kErrGrad, (static_cast<unsigned long long>(q) << 40) | k);
+          acc += static_cast<double>(x);
+        }
+        const float v = static_cast<float>(acc * inv_n);
+        for (int q = 0; q < p.n; ++q) p.peer_out[q][k] = v;
       }
-      const float v = static_cast<float>(acc * inv_n);
-      for (int q = 0; q < p.n; ++q) p.peer_out[q][k] = v;
+    }
+    if (p.pieces > 0) {
+      // Piece delivered: CTA barrier, then one system fence (cumulative over
+      // the CTA's remote stores) and the CTA count; the last CTA raises the flag.
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(p.piece_done + pc, 1u) == gridDim.x - 1) {
+          p.piece_done[pc] = 0u;
+          if (pc == P - 1) {
+            __threadfence();
+            forward_grad_error(p.err, p.peer_err, p.n);  // every rank raises (optimizers.cpp:99-117)
+          }
+          __threadfence_system();
+          for (int q = 0; q < p.n; ++q)
+            st_relaxed_sys(p.peer_flags[q] + p.piece_flag_base + p.rank * p.pieces + pc, p.epoch);
+        }
+      }
     }
   }
   __threadfence_system();  // this thread's remote stores and error reports
@@ -2055,6 +2092,26 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
     forward_grad_error(p.err, p.peer_err, p.n);  // every rank raises (optimizers.cpp:99-117)
     __threadfence_system();
     for (int q = 0; q < p.n; ++q) st_relaxed_sys(p.peer_flags[q] + p.out_flag + p.rank, p.epoch);
+  }
+}
+
+// Consumer side of the piecewise exchange: every rank's piece p delivered.
+__global__ void k_wait_piece(const unsigned long long* flags, int base, int n, int pieces, int pc,
+                             unsigned long long epoch, unsigned long long* err) {
+  if (gate_closed_call(err)) return;
+  if (threadIdx.x == 0) {
+    const unsigned long long bound = wait_bound(err), t0 = now_ns();
+    for (int q = 0; q < n && !gate_closed(err); ++q) {
+      while (ld_acquire_sys(flags + base + q * pieces + pc) < epoch) {
+        if (gate_closed(err)) break;
+        __nanosleep(32);
+        if (now_ns() - t0 > bound) {
+          flag(err, kErrPeer, static_cast<unsigned long long>(q));
+          close_gate(err, kGateMidStep);
+          break;
+        }
+      }
+    }
   }
 }
 
@@ -2857,7 +2914,7 @@ int launch_w1(const W1Params& p, int grid, cudaStream_t s) {
 }
 
 int launch_wepilogue(const WEpiParams& p, cudaStream_t s) {
-  k_wepilogue<<<p.L, 1024, 0, s>>>(p);
+  k_wepilogue<<<p.layer_list ? p.count : p.L, 1024, 0, s>>>(p);
   return 1;
 }
 
@@ -2944,14 +3001,34 @@ int launch_small_collective(const SmallParams& p, int k1_mode, cudaStream_t s) {
   return al ? launch_small_t<2, true>(p, tiles, s) : launch_small_t<2, false>(p, tiles, s);
 }
 
+int lossless_piece(uint64_t lo, uint64_t hi, int pieces, uint64_t k) {
+  const uint64_t up = (lo + 3) & ~3ull, dn = hi & ~3ull;
+  const uint64_t a0 = up < hi ? up : hi;
+  const uint64_t a1 = dn > a0 ? dn : a0;
+  if (k < a0) return 0;
+  if (k >= a1) return pieces - 1;
+  int p = static_cast<int>((k - a0) * static_cast<uint64_t>(pieces) / (a1 - a0));
+  while (p > 0 && k < piece_body_start(a0, a1, pieces, p)) --p;
+  while (p + 1 < pieces && k >= piece_body_start(a0, a1, pieces, p + 1)) ++p;
+  return p;
+}
+
+int launch_wait_piece(const unsigned long long* flags, int base, int n, int pieces, int pc,
+                      unsigned long long epoch, unsigned long long* err, cudaStream_t s) {
+  k_wait_piece<<<1, 32, 0, s>>>(flags, base, n, pieces, pc, epoch, err);
+  return 1;
+}
+
 int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s) {
   const long long groups = static_cast<long long>(p.c / 4) + 1;
-  const int want = static_cast<int>(std::min<long long>((groups + 255) / 256, 8ll * sms));
+  const long long cap = p.ctas > 0 ? p.ctas : 8ll * sms;
+  const int want = static_cast<int>(std::min<long long>((groups + 255) / 256, cap));  // (256-thread estimate)
+  const int bt = p.block > 0 ? p.block : 256;
   switch (p.n) {
-    case 2: k_lossless_p2p<2><<<resident(k_lossless_p2p<2>, want), 256, 0, s>>>(p); break;
-    case 4: k_lossless_p2p<4><<<resident(k_lossless_p2p<4>, want), 256, 0, s>>>(p); break;
-    case 8: k_lossless_p2p<8><<<resident(k_lossless_p2p<8>, want), 256, 0, s>>>(p); break;
-    default: k_lossless_p2p<0><<<resident(k_lossless_p2p<0>, want), 256, 0, s>>>(p); break;
+    case 2: k_lossless_p2p<2><<<resident(k_lossless_p2p<2>, want), bt, 0, s>>>(p); break;
+    case 4: k_lossless_p2p<4><<<resident(k_lossless_p2p<4>, want), bt, 0, s>>>(p); break;
+    case 8: k_lossless_p2p<8><<<resident(k_lossless_p2p<8>, want), bt, 0, s>>>(p); break;
+    default: k_lossless_p2p<0><<<resident(k_lossless_p2p<0>, want), bt, 0, s>>>(p); break;
   }
   return 1;
 }

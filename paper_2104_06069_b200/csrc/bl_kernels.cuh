@@ -143,6 +143,7 @@ struct LayerTiles {
   unsigned int* ctr;            // dynamic tile counter (self-resetting) or nullptr
   const int* order;             // [tiles] processing order (boundary tiles first) or nullptr
   int mis;                      // some full tile lies in a layer not 16-B aligned
+  int count;                    // sub-launch: only order[0..count) (needs ctr and order); 0 = all
 };
 
 struct K5Params {
@@ -224,6 +225,15 @@ struct LosslessP2PParams {
   unsigned long long epoch;
   unsigned int* done;                     // local CTA counter (self-resetting)
   unsigned long long* err;
+  // Piecewise delivery (warmup overlap): the chunk is reduced in `pieces`
+  // consecutive pieces; when every CTA finished piece p, the flag
+  // piece_flag_base + rank * pieces + p is raised at every rank, so the
+  // consumer (W1/W2 sub-launches) starts on the delivered part.  0 = off.
+  int pieces;
+  int piece_flag_base;
+  unsigned int* piece_done;               // [pieces] local CTA counters (self-resetting)
+  int ctas;                               // grid cap (leave SM room for the consumer), 0 = full
+  int block;                              // threads per CTA (0 = 256)
 };
 
 struct W1Params {
@@ -241,6 +251,8 @@ struct W1Params {
 
 struct WEpiParams {
   const unsigned long long* gate;
+  const int* layer_list;  // sub-launch: block b handles layer layer_list[b] (nullptr: block = layer)
+  int count;              // sub-launch: number of layers (0 = L)
   int L;
   const int* layer_tile_start;
   const uint64_t* off;
@@ -327,6 +339,12 @@ int launch_verify(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t
                   uint64_t c, uint64_t len, double tol, unsigned long long* err, cudaStream_t s);
 // Block the stream until flags[0..n) >= epoch (peer signals, bounded wait).
 int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s);
+// Piece boundaries of the piecewise lossless exchange: element k of chunk
+// [lo, hi) (global indices) belongs to piece lossless_piece(lo, hi, pieces, k).
+int lossless_piece(uint64_t lo, uint64_t hi, int pieces, uint64_t k);
+// Block the stream until every rank's piece p is delivered (flags[base + q*pieces + p] >= epoch).
+int launch_wait_piece(const unsigned long long* flags, int base, int n, int pieces, int p,
+                      unsigned long long epoch, unsigned long long* err, cudaStream_t s);
 // Returns 1, or -cudaError when the cooperative launch is refused.
 int launch_small_collective(const SmallParams& p, int k1_mode, cudaStream_t s);
 // Raise flag `index` (+ own rank) at every peer to `epoch` after this stream's

@@ -436,7 +436,9 @@ void bl_cluster::finish_compressed(float es_host, const float* es_dev) {
 void bl_cluster::setup_p2p(bool required) {
   const size_t nn = static_cast<size_t>(n);
   rx = dalloc<uint32_t>(2 * nn * slot);
-  flags = reinterpret_cast<unsigned long long*>(dalloc<double>(5 * nn + 8));
+  flags = reinterpret_cast<unsigned long long*>(
+      dalloc<double>(static_cast<size_t>(piece_flag_base()) + nn * kMaxPieces));
+  piece_done = reinterpret_cast<unsigned int*>(dalloc<float>(kMaxPieces));
   lossless_done = reinterpret_cast<unsigned int*>(dalloc<float>(1));
   small_bar = reinterpret_cast<unsigned int*>(dalloc<float>(2));
   // Buffers every peer maps: packet receive slots, result packets, flags,
@@ -571,6 +573,58 @@ void bl_cluster::lossless(bool check_finite) {
   nccl_check(ncclAllGather(out + static_cast<size_t>(rank) * c, out, c, ncclFloat32, comm, stream),
              "ncclAllGather");
   end(KC_AG, a, 0);
+}
+
+unsigned long long bl_cluster::lossless_pieces(bool check_finite, int pieces) {
+  const unsigned long long ep = ++lcalls;
+  const int nn = n;
+  if (!comm_stream) {
+    cuda_check(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking), "comm stream");
+    cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+  }
+  cudaEvent_t a;
+  begin(KC_A2A, &a);
+  end(KC_A2A, a, launch_signal_peers(d_peer_flags, 2 * nn + rank, nn, ep, err, stream));
+  cuda_check(cudaEventRecord(ev_fork, stream), "fork");
+  cuda_check(cudaStreamWaitEvent(comm_stream, ev_fork, 0), "fork wait");
+  LosslessP2PParams lp{};
+  lp.peer_in = d_peer_in;
+  lp.peer_out = d_peer_out;
+  lp.peer_err = d_peer_err;
+  lp.peer_flags = d_peer_flags;
+  lp.in_flags = flags + 2 * nn;
+  lp.out_flag = 3 * nn;
+  lp.n = nn;
+  lp.rank = rank;
+  lp.check_finite = check_finite ? 1 : 0;
+  lp.c = c;
+  lp.d = dim;
+  lp.epoch = ep;
+  lp.done = lossless_done;
+  lp.err = err;
+  lp.pieces = pieces;
+  lp.piece_flag_base = piece_flag_base();
+  lp.piece_done = piece_done;
+  const char* ce = std::getenv("BL_LOSSLESS_CTAS_PER_SM");
+  lp.ctas = sms * (ce ? std::max(1, std::atoi(ce)) : 1);  // leave the SMs' remaining slots to W1/W2
+  const char* be = std::getenv("BL_LOSSLESS_BLOCK");
+  lp.block = be ? std::atoi(be) : 128;
+  // Launched (and profiled) on the comm stream, concurrent with the consumers.
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (profiling) {
+    e0 = get_event();
+    cuda_check(cudaEventRecord(e0, comm_stream), "cudaEventRecord");
+  }
+  launches += static_cast<uint64_t>(launch_lossless_p2p(lp, sms, comm_stream));
+  cuda_check(cudaGetLastError(), "lossless (pieces)");
+  if (profiling) {
+    e1 = get_event();
+    cuda_check(cudaEventRecord(e1, comm_stream), "cudaEventRecord");
+    pending.push_back({KC_AVG, e0, e1});
+  }
+  cuda_check(cudaEventRecord(ev_join, comm_stream), "join");
+  return ep;
 }
 
 // verify_compensation (comm_sim.cpp:83-106, 145-147, 170-172): after a
@@ -852,14 +906,90 @@ bl::LayerTiles bl_optimizer::lt() const {
           dyn ? tile_order : nullptr, mis_layers ? 1 : 0};
 }
 
+void bl_optimizer::build_piece_tables(int K) {
+  // Lossless piece after which every element of [e0, e1) is delivered: per
+  // chunk the piece of its last element in the range (pieces are monotone).
+  auto req = [&](uint64_t e0, uint64_t e1) {
+    int r = 0;
+    for (uint64_t j = e0 / cl->c; j * cl->c < e1; ++j) {
+      const uint64_t lo = j * cl->c, hi = lo + cl->c;
+      r = std::max(r, lossless_piece(lo, hi, K, std::min(e1, hi) - 1));
+    }
+    return r;
+  };
+  std::vector<int> tpiece(static_cast<size_t>(tiles)), lpiece(static_cast<size_t>(L), 0);
+  std::vector<int> tl_h(static_cast<size_t>(tiles));
+  for (int l = 0; l < L; ++l) {
+    const uint64_t lo = off[l], hi = off[l + 1];
+    int t = 0;
+    for (uint64_t e0 = lo; e0 < hi; e0 += kTile, ++t) {
+      const int tile = lt_start_h[l] + t;
+      tpiece[tile] = req(e0, std::min<uint64_t>(e0 + kTile, hi));
+      tl_h[tile] = l;
+      lpiece[l] = std::max(lpiece[l], tpiece[tile]);
+    }
+  }
+  auto bucket = [&](const std::vector<int>& items, auto key, std::vector<int>& start) {
+    std::vector<std::vector<int>> b(static_cast<size_t>(K));
+    for (int it : items) b[static_cast<size_t>(key(it))].push_back(it);
+    std::vector<int> out;
+    start.assign(static_cast<size_t>(K) + 1, 0);
+    for (int p = 0; p < K; ++p) {
+      start[p] = static_cast<int>(out.size());
+      out.insert(out.end(), b[p].begin(), b[p].end());
+    }
+    start[K] = static_cast<int>(out.size());
+    return out;
+  };
+  const std::vector<int> w1 = bucket(tile_order_h, [&](int t) { return tpiece[t]; }, w1_start);
+  const std::vector<int> w2 = bucket(tile_order_h, [&](int t) { return lpiece[tl_h[t]]; }, w2_start);
+  std::vector<int> layers(static_cast<size_t>(L));
+  for (int l = 0; l < L; ++l) layers[l] = l;
+  const std::vector<int> lw = bucket(layers, [&](int l) { return lpiece[l]; }, lw_start);
+  for (int* p : {w1_order, w2_order, lw_order})
+    if (p) cudaFree(p);
+  w1_order = reinterpret_cast<int*>(dalloc<float>(w1.size()));
+  w2_order = reinterpret_cast<int*>(dalloc<float>(w2.size()));
+  lw_order = reinterpret_cast<int*>(dalloc<float>(lw.size()));
+  cuda_check(cudaMemcpy(w1_order, w1.data(), w1.size() * 4, cudaMemcpyHostToDevice), "w1 order");
+  cuda_check(cudaMemcpy(w2_order, w2.data(), w2.size() * 4, cudaMemcpyHostToDevice), "w2 order");
+  cuda_check(cudaMemcpy(lw_order, lw.data(), lw.size() * 4, cudaMemcpyHostToDevice), "layer order");
+  piece_k = K;
+}
+
 void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, bool adam) {
   // average_lossless (optimizers.cpp:119-138).  With one worker the average
   // (float)((0.0 + g) * 1.0) is g itself: W1 reads the gradient in place and
   // only the finite check runs.
   const bool single = cl->n == 1;
   cudaEvent_t a;
+  // Multi-process over NVLink: the exchange is delivered piece by piece and
+  // W1 / the layer epilogue / W2 follow it (same kernels on tile and layer
+  // subsets), so the NVLink transfer and the HBM-bound update overlap.
+  const char* pe = std::getenv("BL_WARMUP_PIECES");
+  const int K = std::min(bl_cluster::kMaxPieces, pe ? std::max(0, std::atoi(pe)) : 8);
+  const bool overlap = !single && cl->mode == BL_MODE_NCCL && cl->transport == BL_TRANSPORT_P2P && K > 0 &&
+                       std::getenv("BL_STATIC_TILES") == nullptr;
+  if (overlap) {
+    if (piece_k != K) build_piece_tables(K);
+    const unsigned long long ep = cl->lossless_pieces(true, K);
+    cl->ledger_lossless();
+    warmup_kernels(lr, track, finalize, adam, K, ep);
+    cuda_check(cudaStreamWaitEvent(cl->stream, cl->ev_join, 0), "join");
+    return;
+  }
   if (!single) cl->lossless(true);
   cl->ledger_lossless();
+  warmup_kernels(lr, track, finalize, adam, 0, 0);
+}
+
+// W1 -> layer epilogue -> W2 (optimizers.cpp:140-177, 202-224).  K > 0: per
+// lossless piece p, wait for every rank's piece p, then the tiles / layers of
+// that piece (sub-launches of the same kernels; bit-identical results).
+void bl_optimizer::warmup_kernels(double lr, bool track, bool finalize, bool adam, int K,
+                                  unsigned long long ep) {
+  const bool single = cl->n == 1;
+  cudaEvent_t a;
   W1Params w1{};
   w1.gate = cl->err;
   w1.lt = lt();
@@ -877,8 +1007,6 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   w1.adam = adam ? 1 : 0;
   w1.err = single ? cl->err : nullptr;  // check_gradients fused into W1
   w1.worker_base = cl->rank;
-  cl->begin(KC_W1, &a);
-  cl->end(KC_W1, a, launch_w1(w1, cl->grid(tiles), cl->stream));
 
   WEpiParams we{};
   we.gate = cl->err;
@@ -907,8 +1035,6 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   we.finalize = finalize ? 1 : 0;
   we.adam = adam ? 1 : 0;
   we.onebit_adam = variant == BL_ONEBIT_ADAM ? 1 : 0;
-  cl->begin(KC_WEPI, &a);
-  cl->end(KC_WEPI, a, launch_wepilogue(we, cl->stream));
 
   W2Params w2{};
   w2.gate = cl->err;
@@ -921,8 +1047,49 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   w2.eta = static_cast<float>(hp.eta);
   w2.wd = static_cast<float>(hp.weight_decay);
   w2.finalize = finalize ? 1 : 0;
-  cl->begin(KC_W2, &a);
-  cl->end(KC_W2, a, launch_w2(w2, cl->grid(tiles), cl->stream));
+  if (K == 0) {
+    cl->begin(KC_W1, &a);
+    cl->end(KC_W1, a, launch_w1(w1, cl->grid(tiles), cl->stream));
+    cl->begin(KC_WEPI, &a);
+    cl->end(KC_WEPI, a, launch_wepilogue(we, cl->stream));
+    cl->begin(KC_W2, &a);
+    cl->end(KC_W2, a, launch_w2(w2, cl->grid(tiles), cl->stream));
+    return;
+  }
+  const bool consumers = std::getenv("BL_WARMUP_NO_CONSUMERS") == nullptr;  // timing experiments only
+  const char* ev = std::getenv("BL_WARMUP_W2_EVERY");
+  const int every = std::max(1, ev ? std::atoi(ev) : 4);
+  for (int p = 0; p < K; ++p) {
+    if (!consumers) continue;
+    cl->begin(KC_AG, &a);
+    cl->end(KC_AG, a,
+            launch_wait_piece(cl->flags, cl->piece_flag_base(), cl->n, K, p, ep, cl->err, cl->stream));
+    if (const int cnt = w1_start[p + 1] - w1_start[p]) {
+      W1Params q = w1;
+      q.lt.order = w1_order + w1_start[p];
+      q.lt.count = cnt;
+      cl->begin(KC_W1, &a);
+      cl->end(KC_W1, a, launch_w1(q, cl->grid(cnt), cl->stream));
+    }
+    // The layers completed by the last `every` pieces: epilogue, then W2 (batched:
+    // fewer, larger launches; W2 is not needed before the end of the step).
+    if ((p + 1) % every != 0 && p != K - 1) continue;
+    const int b0 = std::max(0, p + 1 - every);
+    if (const int cnt = lw_start[p + 1] - lw_start[b0]) {
+      WEpiParams q = we;
+      q.layer_list = lw_order + lw_start[b0];
+      q.count = cnt;
+      cl->begin(KC_WEPI, &a);
+      cl->end(KC_WEPI, a, launch_wepilogue(q, cl->stream));
+    }
+    if (const int cnt = w2_start[p + 1] - w2_start[b0]) {
+      W2Params q = w2;
+      q.lt.order = w2_order + w2_start[b0];
+      q.lt.count = cnt;
+      cl->begin(KC_W2, &a);
+      cl->end(KC_W2, a, launch_w2(q, cl->grid(cnt), cl->stream));
+    }
+  }
 }
 
 void bl_optimizer::compressed_step(double lr, const float* stage_host) {
@@ -1369,7 +1536,8 @@ void bl_cluster_destroy(bl_cluster* c) {
                   c->scmax,     c->out,        c->lrecv,           c->err,       c->stat_part,
                   c->stat_max,  c->stat_out,   c->rx,              c->flags,     c->d_peer_rx,
                   c->d_peer_res, c->d_peer_flags, c->d_peer_in, c->d_peer_out, c->d_peer_err,
-                  c->lossless_done, c->small_bar, c->k1_slow, c->k1_order, c->tile_ctr};
+                  c->lossless_done, c->small_bar, c->k1_slow, c->k1_order, c->tile_ctr,
+                  c->piece_done,    c->gate_status};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& e : c->pending) {
@@ -1380,6 +1548,12 @@ void bl_cluster_destroy(bl_cluster* c) {
   if (c->copy_stream) {
     for (auto e : c->piece_ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->copy_stream);
+  }
+  if (c->comm_stream) {
+    cudaStreamSynchronize(c->comm_stream);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_join);
+    cudaStreamDestroy(c->comm_stream);
   }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1687,6 +1861,7 @@ static bl_status optimizer_create(int32_t variant, const uint64_t* sizes, const 
       o->layer_tile_start = reinterpret_cast<int*>(dalloc<float>(L + 1));
       cuda_check(cudaMemcpy(o->off_dev, o->off.data(), (L + 1) * 8, cudaMemcpyHostToDevice), "off");
       cuda_check(cudaMemcpy(o->tile_layer, tl.data(), tl.size() * 4, cudaMemcpyHostToDevice), "tiles");
+      o->lt_start_h = tstart;
       cuda_check(cudaMemcpy(o->layer_tile_start, tstart.data(), (L + 1) * 4, cudaMemcpyHostToDevice),
                  "tile start");
       const size_t dn = o->d + kSlack;
@@ -1751,6 +1926,7 @@ static bl_status optimizer_create(int32_t variant, const uint64_t* sizes, const 
           }
         }
         order.insert(order.end(), fast.begin(), fast.end());
+        o->tile_order_h = order;
         o->tile_order = reinterpret_cast<int*>(dalloc<float>(order.size()));
         cuda_check(cudaMemcpy(o->tile_order, order.data(), order.size() * 4, cudaMemcpyHostToDevice),
                    "tile order");
@@ -1809,7 +1985,8 @@ void bl_optimizer_destroy(bl_optimizer* o) {
   void* bufs[] = {o->off_dev, o->tile_layer, o->layer_tile_start, o->x, o->m, o->v, o->vf,
                   o->mprev, o->c_avg, o->r_prev, o->coeff, o->mag, o->A, o->B, o->invc, o->coef_x,
                   o->trace, o->cmean, o->es, o->counter, o->tile_sums, o->tile_max,
-                  o->k1_tile_layer, o->k1_slow, o->k1_order, o->tile_order};
+                  o->k1_tile_layer, o->k1_slow, o->k1_order, o->tile_order,
+                  o->w1_order, o->w2_order, o->lw_order};
   for (void* p : bufs)
     if (p) cudaFree(p);
   delete o;

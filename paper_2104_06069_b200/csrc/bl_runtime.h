@@ -186,6 +186,16 @@ struct bl_cluster {
                   const float* es_dev, float* dec_out = nullptr);
   void finish_compressed(float es_host, const float* es_dev);
   void lossless(bool check_finite);  // in -> out (averaged), ledger
+  // Warmup overlap (P2P, n > 1): the lossless exchange runs on comm_stream,
+  // delivering the result in `pieces` pieces (flags at piece_flag_base); the
+  // caller's consumers wait per piece on the main stream, then join.
+  // Returns the exchange epoch.
+  unsigned long long lossless_pieces(bool check_finite, int pieces);
+  int piece_flag_base() const { return 6 * n + 8; }
+  static constexpr int kMaxPieces = 64;
+  unsigned int* piece_done = nullptr;  // [kMaxPieces]
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void refresh_stats();
   void check_errors(const bl_optimizer* opt);
   void sync_and_check(const bl_optimizer* opt);
@@ -222,6 +232,16 @@ struct bl_optimizer {
   int* k1_order = nullptr;       // K1 processing order, boundary tiles first
   bool frozen = false, has_vf = false, has_mprev = false;
   std::vector<std::string> names;  // layer names (LayerSpec::name) for error messages
+  std::vector<int> tile_order_h;   // host copy of tile_order
+  // Warmup overlap tables (built for the cluster's chunk length and piece
+  // count on first use): tiles / layers bucketed by the lossless piece after
+  // which their data (W1) or their whole layer (epilogue, W2) is delivered.
+  int piece_k = 0;
+  int* w1_order = nullptr;  // [tiles]
+  int* w2_order = nullptr;  // [tiles]
+  int* lw_order = nullptr;  // [L]
+  std::vector<int> w1_start, w2_start, lw_start;  // [piece_k + 1]
+  void build_piece_tables(int pieces);
   bool strict = false;          // read-only finite pre-pass before any mutation (optimizers.cpp:99-117)
   bool m_valid = true;          // m buffer holds m (else: decompressed result * invc)
   bool mprev_separate = false;  // m_prev poked by the caller
@@ -234,6 +254,8 @@ struct bl_optimizer {
   void step(const float* const* grads, int n_grads, uint64_t t, double lr, int memory,
             bl_step_trace* trace_out);
   void warmup_step(uint64_t t, double lr, bool track, bool finalize, bool adam);
+  void warmup_kernels(double lr, bool track, bool finalize, bool adam, int pieces, unsigned long long ep);
+  std::vector<int> lt_start_h;  // host copy of layer_tile_start
   void compressed_step(double lr, const float* stage_host);
   void materialize_m(float* dst);
 };
