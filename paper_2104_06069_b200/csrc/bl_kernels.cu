@@ -2402,53 +2402,279 @@ __device__ __forceinline__ void k3_cta_tile(const K3Params& p, long long tile, u
   __syncthreads();
 }
 
+// ---- LL transport of the fused small collective ------------------------------
+__device__ __forceinline__ uint2 ld_ll(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
+// 4 packet words -> 4 LL words (word, epoch), two 16-byte stores.
+__device__ __forceinline__ void st_ll4(uint2* dst, const uint4& w, uint32_t ep) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(w.x), "r"(ep), "r"(w.y), "r"(ep)
+               : "memory");
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst + 2), "r"(w.z), "r"(ep), "r"(w.w),
+               "r"(ep)
+               : "memory");
+}
+__device__ __forceinline__ void st_ll1(uint2* dst, uint32_t w, uint32_t ep) {
+  asm volatile("st.volatile.global.v2.u32 [%0], {%1,%2};" ::"l"(dst), "r"(w), "r"(ep) : "memory");
+}
+// The word of an LL slot once it carries `ep` (fail-stop bound as wait_peers).
+__device__ __forceinline__ uint32_t ll_get(const uint2* p, uint32_t ep, unsigned long long* err, bool& ok) {
+  uint2 v = ld_ll(p);
+  if (v.y == ep) return v.x;
+  const unsigned long long t0 = now_ns(), bound = wait_bound(err);
+  for (int it = 0;; ++it) {
+    v = ld_ll(p);
+    if (v.y == ep) return v.x;
+    if ((it & 63) == 63) {
+      if (gate_closed(err)) break;
+      if (now_ns() - t0 > bound) {
+        close_gate(err, kGateMidStep);
+        break;
+      }
+    }
+  }
+  ok = false;
+  return 0u;
+}
+
+// One K3 tile per CTA over LL-received worker words (k3_cta_tile's arithmetic
+// and order); server words go to the local plain result slot and, as LL
+// words, to every rank's result buffer.
+__device__ __forceinline__ void k3_cta_tile_ll(const SmallParams& sp, long long tile, uint32_t* sw, float* s_abs,
+                                               float* s_cm, const float* scale, float es, double inv_n,
+                                               bool& ok) {
+  const K3Params& p = sp.k3;
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int n = p.n;
+  const int t = static_cast<int>(tile);
+  const int j = p.server_base;
+  const uint64_t i0 = static_cast<uint64_t>(t) * kTile;
+  float* se = p.serr + i0;
+  const uint32_t* rs = p.res_prev + static_cast<size_t>(j) * p.slot;
+  const float S2p = slot_scale(rs, p.W);
+  rs += i0 >> 5;
+  const uint2* inw = sp.ll_rx_mine + (i0 >> 5);
+  constexpr int R = 4;
+  const int r0 = R * wq;
+  constexpr int kMaxN = 8;
+  float4 raw[R];
+  uint32_t sn[R], nb[R][kMaxN];
+  uint2 lv[R][kMaxN];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {  // every load of the tile in flight at once, then the epoch checks
+    raw[k] = ld4(se + (r0 + k) * kRowElems + 4 * lane);
+    sn[k] = row_nibble(rs, r0 + k, lane);
+#pragma unroll
+    for (int i = 0; i < kMaxN; ++i)
+      lv[k][i] = i < n ? ld_ll(inw + i * p.slot + 4 * (r0 + k) + (lane >> 3)) : make_uint2(0u, sp.ep32);
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+#pragma unroll
+    for (int i = 0; i < kMaxN; ++i)
+      nb[k][i] = lv[k][i].y == sp.ep32 ? lv[k][i].x
+                                       : ll_get(inw + i * p.slot + 4 * (r0 + k) + (lane >> 3), sp.ep32, sp.err, ok);
+  float cm = 0.0f;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int r = r0 + k;
+    const uint64_t ir = i0 + static_cast<uint64_t>(r) * kRowElems;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    auto add = [&](int i, uint32_t word) {  // compression.cpp:83-89, ascending workers
+      const float S = scale[i];
+      const uint32_t b = (word >> (4 * (lane & 7))) & 0xFu;
+      if (S != 0.0f) {
+        const double Sd = S;
+        a0 += (b & 1u) ? Sd : -Sd;
+        a1 += (b & 2u) ? Sd : -Sd;
+        a2 += (b & 4u) ? Sd : -Sd;
+        a3 += (b & 8u) ? Sd : -Sd;
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < kMaxN; ++i)
+      if (i < n) add(i, nb[k][i]);
+    for (int i = kMaxN; i < n; ++i) add(i, ll_get(inw + i * p.slot + 4 * r + (lane >> 3), sp.ep32, sp.err, ok));
+    const float4 avg = make_float4(static_cast<float>(a0 * inv_n), static_cast<float>(a1 * inv_n),
+                                   static_cast<float>(a2 * inv_n), static_cast<float>(a3 * inv_n));
+    uint32_t nib = 0;
+    float4 rawn, ab;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = ir + 4 * lane + q;
+      const float v = comp(avg, q);
+      const float rec = (sn[k] >> q) & 1u ? S2p : -S2p;
+      const float delta = __fsub_rn(comp(raw[k], q), rec);
+      const float corr = __fadd_rn(v, __fmul_rn(es, delta));
+      const bool live = i < p.c;
+      set_comp(rawn, q, live ? __fadd_rn(v, delta) : 0.0f);
+      nib |= static_cast<uint32_t>(live && corr >= 0.0f) << q;
+      set_comp(ab, q, live ? fabsf(corr) : 0.0f);
+      if (live) cm = cm < fabsf(corr) ? fabsf(corr) : cm;
+    }
+    if (ok && ir < p.c) st4(se + r * kRowElems + 4 * lane, rawn);
+    *reinterpret_cast<float4*>(s_abs + r * kRowElems + 4 * lane) = ab;
+    stage_row_bits(sw, r, lane, nib);
+  }
+  cm = warp_max(cm);
+  if (lane == 0) s_cm[wq] = cm;
+  __syncthreads();
+  if (wq == 0) {
+    double acc = 0.0;
+    for (int r = 0; r < kRowsPerTile; ++r) {
+      const float4 ab = *reinterpret_cast<const float4*>(s_abs + r * kRowElems + 4 * lane);
+      acc += static_cast<double>(ab.x);
+      acc += static_cast<double>(ab.y);
+      acc += static_cast<double>(ab.z);
+      acc += static_cast<double>(ab.w);
+    }
+    acc = warp_bfly_sum(acc);
+    if (lane == 0) p.partials[t] = acc;
+    if (p.cmax) {
+      const float m = warp_max(lane < kWarpsPerBlock ? s_cm[lane] : 0.0f);
+      if (lane == 0) p.cmax[t] = m;
+    }
+    const uint4 v = tile_words(sw, lane);
+    reinterpret_cast<uint4*>(p.res_cur + static_cast<size_t>(j) * p.slot + (i0 >> 5))[lane] = v;
+    for (int q = 0; q < n; ++q) st_ll4(sp.ll_res[q] + sp.ll_off + (i0 >> 5) + 4 * lane, v, sp.ep32);
+  }
+  __syncthreads();
+}
+
+// True in every thread of the CTA that arrives last at counter `c` (after
+// its own global writes; gpu-scope fence + count); that CTA resets it.
+__device__ __forceinline__ bool last_cta(unsigned int* c, bool* s_last) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    *s_last = atomicAdd(c, 1u) == gridDim.x - 1;
+    if (*s_last) {
+      *c = 0u;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return *s_last;
+}
+
+// ---------------------------------------------------------------------------
+// Fused small compressed collective (P2P transport): K1 -> worker scales ->
+// exchange -> K3 -> server scale -> exchange [-> decompress] in one
+// cooperative kernel.  Below ~32 MB per rank the separate kernels are
+// latency-bound; here nothing waits on a grid barrier, a system fence or a
+// flag: packet words and scales travel as LL words (word + epoch in one
+// 8-byte store), each consumer polls exactly the words it needs, and each
+// scale is formed by the CTA that finishes its phase last (last-CTA count).
+// Every per-element operation and reduction order is the unfused path's.
+// ---------------------------------------------------------------------------
 template <int MODE, bool ALIGNED>
 __global__ void __launch_bounds__(kBlock) k_small_collective(__grid_constant__ const SmallParams p) {
   __shared__ __align__(16) uint32_t s_words[128];  // the CTA's tile packet words
   __shared__ float s_scale[64];
-  __shared__ uint32_t* s_peer[64];
   __shared__ double s_red[1024 + 32];
   __shared__ __align__(16) float s_abs[kTile];
   __shared__ float s_cm[kWarpsPerBlock];
+  __shared__ bool s_last;
+  __shared__ int s_ok;
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
-  if (gate_closed_call(p.err)) return;  // every CTA: the grid barriers stay balanced
+  if (gate_closed_call(p.err)) return;
+  auto stamp = [&](int k) {
+    if (p.ts && blockIdx.x == 0 && threadIdx.x == 0) p.ts[k] = now_ns();
+  };
+  stamp(0);
   const int n = p.k1.n;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) s_peer[q] = p.k3.peer_res[q];
-  // 1. worker compression of every chunk of the local stream; packet words
-  //    go to the local slot and into rank j's receive slot
+  const uint32_t ep = p.ep32;
+  bool ok = true;
+  // 1. worker compression of every chunk of the local stream (plain words to
+  //    the local slot, LL words into rank j's receive buffer)
   {
     const float es = p.k1.es_dev ? __ldg(p.k1.es_dev) : p.k1.es_host;
     const long long total = static_cast<long long>(n) * p.k1.tpc;
-    for (long long tile = blockIdx.x; tile < total; tile += gridDim.x)
+    for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
       k1_cta_tile<MODE, ALIGNED>(p.k1, tile, s_words, s_abs, s_cm, es);
-    warp_fence_system(lane);
+      if (threadIdx.x < 32) {  // the tile's words, just written by this warp
+        const int j = static_cast<int>(tile / p.k1.tpc);
+        const uint64_t w0 = static_cast<uint64_t>(tile - static_cast<long long>(j) * p.k1.tpc) * (kTile / 32);
+        const uint4 v = reinterpret_cast<const uint4*>(p.k1.pk_cur + static_cast<size_t>(j) * p.k1.slot + w0)[lane];
+        st_ll4(p.ll_rx[j] + p.ll_off + w0 + 4 * lane, v, ep);
+      }
+    }
   }
-  grid_barrier(p.bar, gridDim.x, p.err);
-  // 2. worker scales: block e finalizes endpoint (this worker, chunk e) and
-  //    raises rank e's flag
-  for (int e = blockIdx.x; e < n; e += gridDim.x) finalize_block256(p.f1, e, s_red);
-  // 3. every worker's packet for this rank's chunk has arrived (a peer
-  //    timeout closes the gate: the rest is skipped, the barriers still run)
-  const bool live = wait_peers(p.flags, n, p.epoch, p.err);
-  // 4. server reduce of chunk `rank`; server words into every rank's result slot
-  if (live) {
+  stamp(1);
+  // 2. worker scales: the last CTA combines every endpoint's tile partials
+  //    (k_finalize_scales' order) and sends scale e to rank e
+  if (last_cta(p.cnt, &s_last)) {
+    stamp(2);
+    if (threadIdx.x == 0) forward_grad_error(p.err, p.f1.peer_err, n);  // every rank raises
+    for (int e = 0; e < n; ++e) {
+      finalize_block256(p.f1, e, s_red);
+      if (threadIdx.x == 0)
+        st_ll1(p.ll_rx[e] + p.ll_off + p.k1.W, p.k1.pk_cur[static_cast<size_t>(e) * p.k1.slot + p.k1.W], ep);
+    }
+  }
+  stamp(3);
+  // 3./4. server reduce of chunk `rank` from the LL-received worker packets
+  {
+    if (threadIdx.x == 0) s_ok = 1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      bool ok_i = true;
+      s_scale[i] = __uint_as_float(ll_get(p.ll_rx_mine + static_cast<size_t>(i) * p.k3.slot + p.k3.W, ep, p.err, ok_i));
+      if (!ok_i) s_ok = 0;
+    }
+    __syncthreads();
+    ok = s_ok != 0;
+    stamp(4);
     const float es = p.k3.es_dev ? __ldg(p.k3.es_dev) : p.k3.es_host;
     const double inv_n = 1.0 / static_cast<double>(n);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s_scale[i] = slot_scale_cg(p.k3.in + i * p.k3.in_i, p.k3.W);
-    __syncthreads();
-    for (long long tile = blockIdx.x; tile < p.k3.tpc; tile += gridDim.x)
-      k3_cta_tile(p.k3, tile, s_words, s_abs, s_cm, s_scale, s_peer, es, inv_n);
-    warp_fence_system(lane);
+    for (long long tile = blockIdx.x; ok && tile < p.k3.tpc; tile += gridDim.x)
+      k3_cta_tile_ll(p, tile, s_words, s_abs, s_cm, s_scale, es, inv_n, ok);
   }
-  grid_barrier(p.bar, gridDim.x, p.err);
-  // 5. server scale to every rank, flags
-  if (live && blockIdx.x == 0) finalize_block256(p.f2, 0, s_red);
-  // 6. every rank's server packet has arrived; 7. optional decompress
-  if (live && wait_peers(p.flags + n, n, p.epoch, p.err) && p.out)
-    decompress_warps(p.res, n, p.k3.c, p.k3.slot, p.k3.W, p.d, p.out, static_cast<uint64_t>(gw),
-                     static_cast<uint64_t>(nwarps), lane);
+  stamp(5);
+  // 5. server scale: the last CTA combines the partials, sends it to every rank
+  if (last_cta(p.cnt + 1, &s_last) && !gate_closed(p.err)) {
+    stamp(6);
+    finalize_block256(p.f2, 0, s_red);
+    if (threadIdx.x == 0) {
+      const uint32_t S = p.res_plain[static_cast<size_t>(p.k3.server_base) * p.k3.slot + p.k3.W];
+      for (int q = 0; q < n; ++q) st_ll1(p.ll_res[q] + p.ll_off + p.k3.W, S, ep);
+    }
+  }
+  stamp(7);
+  // 6./7. every rank's server packet: LL -> plain result slots (K5/K6 read
+  //    them), and the optional decompress (compression.cpp:68-81)
+  {
+    const uint64_t W = p.k3.W, slot = p.k3.slot, c = p.k3.c;
+    const uint64_t groups = (W + 31) / 32;
+    for (uint64_t g = gw; ok && g < groups * n; g += nwarps) {
+      const uint64_t j = g / groups, w0 = (g - j * groups) * 32;
+      const uint2* ll = p.ll_res_mine + j * slot;
+      const uint2 lw = ld_ll(ll + w0 + lane), ls = ld_ll(ll + W);
+      const uint32_t mine = lw.y == ep ? lw.x : ll_get(ll + w0 + lane, ep, p.err, ok);
+      const float S = __uint_as_float(ls.y == ep ? ls.x : ll_get(ll + W, ep, p.err, ok));
+      if (!ok) break;
+      uint32_t* pl = p.res_plain + j * slot;
+      if (static_cast<int>(j) != p.k3.server_base) {
+        pl[w0 + lane] = mine;
+        if (w0 == 0 && lane == 0) pl[W] = __float_as_uint(S);
+      }
+      if (p.out) {
+        const float pos = S, neg = S == 0.0f ? 0.0f : -S;
+        const uint64_t kc = j * c;
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t word = __shfl_sync(FULL, mine, i);
+          const uint64_t e = (w0 + i) * 32 + lane;
+          if (e < c && kc + e < p.d) p.out[kc + e] = (word >> lane) & 1u ? pos : neg;
+        }
+      }
+    }
+  }
+  stamp(8);
 }
 
 __global__ void k_materialize_error(const float* raw, uint64_t c_pad, const uint32_t* pk,

@@ -210,6 +210,18 @@ struct SmallParams {
   float* out;          // decompressed result [d] or nullptr
   const uint32_t* res; // result packets [n][slot] (this call's)
   uint64_t d;
+  unsigned long long* ts;  // phase timestamps (block 0 / the finalizing block) or nullptr
+  // LL ("low latency") transport: every 4-byte packet word travels with the
+  // call's 32-bit epoch in one 8-byte store, so the receiver polls the data
+  // itself -- no system fences, no flag round trips.
+  uint2* const* ll_rx;      // [n] every rank's LL receive buffer [2][n][slot] (worker packets)
+  uint2* const* ll_res;     // [n] every rank's LL result buffer [2][n][slot] (server packets)
+  uint64_t ll_off;          // (parity * n + rank) * slot: this rank's slot at every peer
+  const uint2* ll_rx_mine;  // this rank's LL rx, current parity, [n][slot]
+  const uint2* ll_res_mine; // this rank's LL res, current parity, [n][slot]
+  uint32_t* res_plain;      // this call's plain result packets [n][slot] (K5/K6, getters)
+  unsigned int* cnt;        // [2] CTA counters of the two last-CTA finalizes (self-resetting)
+  unsigned int ep32;
 };
 
 // Deterministic lossless all-reduce over NVLink peer memory (P2P transport).

@@ -203,9 +203,7 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
   // Small collectives over NVLink: one cooperative kernel for the whole
   // exchange (and the decompress, when asked).  BL_SMALL_MAX_TILES sets the
   // size limit (K1 tiles per rank; 0 disables).
-  const char* sm_env = std::getenv("BL_SMALL_MAX_TILES");
-  const long long small_max = sm_env ? std::atoll(sm_env) : 2048;
-  if (p2p && nw == 1 && static_cast<long long>(n) * tpc <= small_max) {
+  if (p2p && nw == 1 && static_cast<long long>(n) * tpc <= small_max_tiles()) {
     if (host) {  // small: copy the staged host gradient first
       const float* srcs[1] = {host};
       copy_inputs(srcs, 1, dim, BL_MEM_HOST);
@@ -215,15 +213,10 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
     sp.k1.slow_list = nullptr;  // every tile through k1_tile
     sp.k1.n_slow = 0;
     sp.k1.skip_fast = 0;
+    sp.k1.peer_rx = nullptr;    // the kernel sends the words as LL words itself
     sp.f1 = FinalizeParams{wpart, tpc, c, wpk[cur()], slot, W, err, p.worker_base * n};
-    sp.f1.peer_slots = d_peer_rx;
-    sp.f1.peer_off = my_slot;
-    sp.f1.peer_flags = d_peer_flags;
-    sp.f1.flag_index = rank;
-    sp.f1.to_all = 0;
     sp.f1.n = n;
-    sp.f1.epoch = epoch;
-    sp.f1.peer_err = d_peer_err;
+    sp.f1.peer_err = d_peer_err;  // (scales travel as LL words: no peer slots/flags here)
     K3Params& k3 = sp.k3;
     k3.n = n;
     k3.ns = 1;
@@ -244,18 +237,10 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
     k3.partials = spart;
     k3.cmax = cfg.endpoint_stats ? scmax : nullptr;
     k3.err = err;
-    k3.peer_res = d_peer_res;
-    k3.res_off = my_slot;
     k3.rank = rank;
     sp.f2 = FinalizeParams{spart, tpc, c, res[cur()] + static_cast<size_t>(rank) * slot, slot, W, err,
                            1 << 20};
-    sp.f2.peer_slots = d_peer_res;
-    sp.f2.peer_off = my_slot;
-    sp.f2.peer_flags = d_peer_flags;
-    sp.f2.flag_index = n + rank;
-    sp.f2.to_all = 1;
     sp.f2.n = n;
-    sp.f2.epoch = epoch;
     sp.flags = flags;
     sp.epoch = epoch;
     sp.err = err;
@@ -263,11 +248,32 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
     sp.out = dec_out;
     sp.res = res[cur()];
     sp.d = dim;
+    sp.ll_rx = d_peer_llrx;
+    sp.ll_res = d_peer_llres;
+    sp.ll_off = my_slot;
+    sp.ll_rx_mine = ll_rx + static_cast<size_t>(cur()) * n * slot;
+    sp.ll_res_mine = ll_res + static_cast<size_t>(cur()) * n * slot;
+    sp.res_plain = res[cur()];
+    sp.cnt = small_bar;
+    sp.ep32 = static_cast<unsigned int>(epoch);
+    // BL_SMALL_TS=1: phase timestamps of block 0 (ns, relative), printed to
+    // stderr after the call -- a latency-analysis aid, synchronizes the stream.
+    static const bool ts_on = std::getenv("BL_SMALL_TS") != nullptr;
+    if (ts_on && !small_ts) small_ts = reinterpret_cast<unsigned long long*>(dalloc<double>(16));
+    sp.ts = ts_on ? small_ts : nullptr;
     begin(KC_SMALL, &a);
     const int r = launch_small_collective(sp, k1_mode, stream);
     if (r < 0) fail(BL_ERR_CUDA, std::string("fused small collective launch: ") +
                                     cudaGetErrorString(static_cast<cudaError_t>(-r)));
     end(KC_SMALL, a, r);
+    if (ts_on) {
+      unsigned long long h[9];
+      cuda_check(cudaMemcpyAsync(h, small_ts, sizeof h, cudaMemcpyDeviceToHost, stream), "ts");
+      cuda_check(cudaStreamSynchronize(stream), "ts");
+      std::fprintf(stderr, "small_ts rank %d tiles %lld:", rank, static_cast<long long>(n) * tpc);
+      for (int k = 1; k < 9; ++k) std::fprintf(stderr, " %.2f", (h[k] - h[0]) * 1e-3);
+      std::fprintf(stderr, "\n");
+    }
     finish_compressed(es_host, es_dev);
     return dec_out != nullptr;
   }
@@ -441,10 +447,16 @@ void bl_cluster::setup_p2p(bool required) {
   piece_done = reinterpret_cast<unsigned int*>(dalloc<float>(kMaxPieces));
   lossless_done = reinterpret_cast<unsigned int*>(dalloc<float>(1));
   small_bar = reinterpret_cast<unsigned int*>(dalloc<float>(2));
+  // LL buffers of the fused small collective, [2][n][slot] (word, epoch)
+  // pairs; only sized when the small path can be taken.
+  const size_t ll_words = static_cast<long long>(n) * tpc <= small_max_tiles() ? 2 * nn * slot : 1;
+  ll_rx = reinterpret_cast<uint2*>(dalloc<double>(ll_words));
+  ll_res = reinterpret_cast<uint2*>(dalloc<double>(ll_words));
   // Buffers every peer maps: packet receive slots, result packets, flags,
-  // gradient (lossless reads), output (lossless allgather), error words.
-  constexpr int kB = 6;
-  void* const local[kB] = {rx, res_base, flags, in, out, err};
+  // gradient (lossless reads), output (lossless allgather), error words,
+  // LL receive slots, LL result slots.
+  constexpr int kB = 8;
+  void* const local[kB] = {rx, res_base, flags, in, out, err, ll_rx, ll_res};
   constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
   std::vector<uint8_t> mine(kB * kH);
   for (int k = 0; k < kB; ++k) {
@@ -504,6 +516,8 @@ void bl_cluster::setup_p2p(bool required) {
   d_peer_in = reinterpret_cast<float**>(table(3));
   d_peer_out = reinterpret_cast<float**>(table(4));
   d_peer_err = reinterpret_cast<unsigned long long**>(table(5));
+  d_peer_llrx = reinterpret_cast<uint2**>(table(6));
+  d_peer_llres = reinterpret_cast<uint2**>(table(7));
   transport = BL_TRANSPORT_P2P;
 }
 
@@ -740,7 +754,9 @@ void bl_cluster::begin_step(bl_optimizer* opt, uint64_t t, bool is_step, bool st
   if (snaps.size() >= 4096) snaps.erase(snaps.begin());  // unsynchronized for that long: keep the tail
   snaps.push_back(sn);
 
-  const bool multi = mode == BL_MODE_NCCL && n > 1;
+  // The arrival barrier guards optimizer steps (abort before any mutation);
+  // a bare collective relies on the fail-stop bound of its own peer waits.
+  const bool multi = mode == BL_MODE_NCCL && n > 1 && is_step;
   if (!strict_check && !multi) return;
   cudaEvent_t a;
   if (strict_check) {  // check_gradients (optimizers.cpp:99-117) before any mutation
@@ -1537,7 +1553,8 @@ void bl_cluster_destroy(bl_cluster* c) {
                   c->stat_max,  c->stat_out,   c->rx,              c->flags,     c->d_peer_rx,
                   c->d_peer_res, c->d_peer_flags, c->d_peer_in, c->d_peer_out, c->d_peer_err,
                   c->lossless_done, c->small_bar, c->k1_slow, c->k1_order, c->tile_ctr,
-                  c->piece_done,    c->gate_status};
+                  c->piece_done,    c->gate_status, c->ll_rx, c->ll_res, c->d_peer_llrx,
+                  c->d_peer_llres,  c->small_ts};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& e : c->pending) {

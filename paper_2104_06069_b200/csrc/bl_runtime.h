@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -99,6 +100,20 @@ struct bl_cluster {
   unsigned long long** d_peer_err = nullptr;  // [n] peers' error words
   unsigned int* lossless_done = nullptr;
   unsigned int* small_bar = nullptr;  // grid barrier of the fused small collective
+  unsigned long long* small_ts = nullptr;  // BL_SMALL_TS phase timestamps
+  uint2* ll_rx = nullptr;              // [2][n][slot] LL worker packets addressed to this rank
+  uint2* ll_res = nullptr;             // [2][n][slot] LL server packets
+  uint2** d_peer_llrx = nullptr;       // [n]
+  uint2** d_peer_llres = nullptr;      // [n]
+  // Collectives of at most this many K1 tiles per rank take the fused
+  // small-collective kernel (BL_SMALL_MAX_TILES; 0 disables).
+  static long long small_max_tiles() {
+    static const long long v = [] {
+      const char* e = std::getenv("BL_SMALL_MAX_TILES");
+      return e ? std::atoll(e) : 2048ll;
+    }();
+    return v;
+  }
   unsigned long long lcalls = 0;      // lossless collectives run (flag epoch)
   // Step gate (bl_kernels.cuh GateParams): arrival words at flags[4n + q],
   // rank 0's decision word at flags[5n].
