@@ -623,7 +623,7 @@ unsigned long long bl_cluster::lossless_pieces(bool check_finite, int pieces) {
   const char* ce = std::getenv("BL_LOSSLESS_CTAS_PER_SM");
   lp.ctas = sms * (ce ? std::max(1, std::atoi(ce)) : 1);  // leave the SMs' remaining slots to W1/W2
   const char* be = std::getenv("BL_LOSSLESS_BLOCK");
-  lp.block = be ? std::atoi(be) : 128;
+  lp.block = be ? std::atoi(be) : (n == 2 ? 256 : 128);
   // Launched (and profiled) on the comm stream, concurrent with the consumers.
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (profiling) {
@@ -983,7 +983,8 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   // W1 / the layer epilogue / W2 follow it (same kernels on tile and layer
   // subsets), so the NVLink transfer and the HBM-bound update overlap.
   const char* pe = std::getenv("BL_WARMUP_PIECES");
-  const int K = std::min(bl_cluster::kMaxPieces, pe ? std::max(0, std::atoi(pe)) : 8);
+  // Defaults from the N=2 / N=4 sweeps (profiles/round2_warm_sweep*.txt).
+  const int K = std::min(bl_cluster::kMaxPieces, pe ? std::max(0, std::atoi(pe)) : (cl->n == 2 ? 4 : 8));
   const bool overlap = !single && cl->mode == BL_MODE_NCCL && cl->transport == BL_TRANSPORT_P2P && K > 0 &&
                        std::getenv("BL_STATIC_TILES") == nullptr;
   if (overlap) {
