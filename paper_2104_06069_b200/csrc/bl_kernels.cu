@@ -1315,6 +1315,13 @@ __device__ __forceinline__ uint32_t nibble_at(const uint32_t* sl, uint32_t i) {
   return __funnelshift_r(w0, w1, i & 31u) & 0xFu;
 }
 
+// Store the lane's first nvl (0..4) elements at p (p may sit off a 16-B boundary).
+__device__ __forceinline__ void st_first(float* p, const float4& v, int nvl) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q < nvl) p[q] = comp(v, q);
+}
+
 __device__ __forceinline__ int lane_valid(uint64_t len, uint64_t ir, int lane) {
   const uint64_t st = ir + 4 * lane;
   if (st >= len) return 0;
@@ -1356,10 +1363,15 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
     uint64_t j = base / p.c, ce = (j + 1) * p.c;
     uint64_t jp = j, cep = ce;
 
-    if ((MISK || s == 0) && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce &&
-        !p.dense && !p.norm_only) {
-      // Fast path: full tile, one chunk of the result (MISK: any layer alignment).
+    const uint64_t tvalid = len - static_cast<uint64_t>(t) * kTile < kTile ? len - static_cast<uint64_t>(t) * kTile
+                                                                          : static_cast<uint64_t>(kTile);
+    if ((MISK || s == 0) && base + tvalid <= ce && !p.dense && !p.norm_only) {
+      // Fast path: one chunk of the result (MISK: any layer alignment).  A
+      // layer's partial last tile takes it too, rows past the layer end
+      // skipped and the last row masked (loads past it stay in the slack).
       constexpr int R = K5_ROWS;
+      const bool part = tvalid < static_cast<uint64_t>(kTile);
+      const int rows_valid = static_cast<int>((tvalid + kRowElems - 1) / kRowElems);
       const uint32_t* sl = cur.res + j * p.slot;
       const float S = slot_scale_cg(sl, p.W);
       const float pos = S, neg = S == 0.0f ? 0.0f : -S;
@@ -1374,9 +1386,10 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
       double acc = 0.0;
       float mx = 0.0f;
       bool bad = false;
-      auto rows = [&](auto mis) {
+      auto rows = [&](auto mis, auto partial) {
         constexpr bool MIS = decltype(mis)::value;
-        for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        constexpr bool PART = decltype(partial)::value;
+        for (int r0 = 0; r0 < (PART ? rows_valid : kRowsPerTile); r0 += R) {
           float4 v[R], vf[R], mpb[R];
           uint32_t nc[R], np[R];
 #pragma unroll
@@ -1390,6 +1403,7 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
           }
 #pragma unroll
           for (int k = 0; k < R; ++k) {
+            const int nvl = PART ? lane_valid(tvalid, static_cast<uint64_t>(r0 + k) * kRowElems, lane) : 4;
             float4 vn;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -1399,21 +1413,37 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
               const float nvv = __fadd_rn(__fmul_rn(p.b2, comp(v[k], q)),
                                           __fmul_rn(__fmul_rn(p.omb2, rec), rec));
               set_comp(vn, q, nvv);
-              bad |= !isfinite(rec);
-              const float den = nvv < p.floor_ ? p.floor_ : nvv;
-              const float ratio = fabsf(comp(vf[k], q)) / den;
-              mx = mx < ratio ? ratio : mx;
-              acc += static_cast<double>(nvv) * static_cast<double>(nvv);
+              if (!PART || q < nvl) {
+                bad |= !isfinite(rec);
+                const float den = nvv < p.floor_ ? p.floor_ : nvv;
+                const float ratio = fabsf(comp(vf[k], q)) / den;
+                mx = mx < ratio ? ratio : mx;
+                acc += static_cast<double>(nvv) * static_cast<double>(nvv);
+              }
             }
-            st_s<MIS>(p.v + base + (r0 + k) * kRowElems + 4 * lane, s, vn);
+            float* dst = p.v + base + (r0 + k) * kRowElems + 4 * lane;
+            if (!PART || nvl == 4) {
+              st_s<MIS>(dst, s, vn);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (q < nvl) dst[q] = comp(vn, q);
+            }
           }
         }
       };
+      // MIS accessors only for a layer off a 16-B boundary (they assume s != 0)
       if constexpr (MISK) {
-        if (s != 0) rows(Mis<true>{});
-        else rows(Mis<false>{});
+        if (s != 0) {
+          if (part) rows(Mis<true>{}, Mis<true>{});
+          else rows(Mis<true>{}, Mis<false>{});
+        } else {
+          if (part) rows(Mis<false>{}, Mis<true>{});
+          else rows(Mis<false>{}, Mis<false>{});
+        }
       } else {
-        rows(Mis<false>{});
+        if (part) rows(Mis<false>{}, Mis<true>{});
+        else rows(Mis<false>{}, Mis<false>{});
       }
       if (bad) flag(p.err, kErrRecon, static_cast<unsigned long long>(l));
       acc = warp_bfly_sum(acc);
@@ -1556,7 +1586,10 @@ __global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
 // K6 — update pass B (optimizers.cpp:308-313): u = m_g/(sqrt(vf)+eta) [+wd x],
 // x += (-lr*c)*u, with m_g recomputed from the result packets.
 template <bool MISK>
-__global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
+#ifndef K6_MINB
+#define K6_MINB 1
+#endif
+__global__ void __launch_bounds__(kBlock, K6_MINB) k6_update_b(const K6Params p) {
   if (gate_closed_call(p.gate)) return;
   const int lane = threadIdx.x & 31;
   const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1573,16 +1606,22 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
     const float ic = __ldg(p.invc + l);
     const float a = __ldg(p.coef_x + l);
     uint64_t j = base / p.c, ce = (j + 1) * p.c;
-    if ((MISK || s == 0) && static_cast<uint64_t>(t + 1) * kTile <= len && base + kTile <= ce &&
-        !p.dense) {
+    const uint64_t tvalid = len - static_cast<uint64_t>(t) * kTile < kTile ? len - static_cast<uint64_t>(t) * kTile
+                                                                          : static_cast<uint64_t>(kTile);
+    if ((MISK || s == 0) && base + tvalid <= ce && !p.dense) {
+      // One chunk of the result; a partial last tile skips the rows past the
+      // layer end and masks its last row (K5's fast path, same treatment).
       constexpr int R = 4;
+      const bool part = tvalid < static_cast<uint64_t>(kTile);
+      const int rows_valid = static_cast<int>((tvalid + kRowElems - 1) / kRowElems);
       const uint32_t* sl = cur.res + j * p.slot;
       const float S = slot_scale(sl, p.W);
       const float pos = S, neg = S == 0.0f ? 0.0f : -S;
       const uint32_t ib = static_cast<uint32_t>(base - j * p.c) + 4 * lane;
-      auto rows = [&](auto mis) {
+      auto rows = [&](auto mis, auto partial) {
         constexpr bool MIS = decltype(mis)::value;
-        for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        constexpr bool PART = decltype(partial)::value;
+        for (int r0 = 0; r0 < (PART ? rows_valid : kRowsPerTile); r0 += R) {
           float4 x[R], vf[R];
           uint32_t nc[R];
 #pragma unroll
@@ -1601,15 +1640,30 @@ __global__ void __launch_bounds__(kBlock) k6_update_b(const K6Params p) {
               if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
               set_comp(xn, q, __fadd_rn(comp(x[k], q), __fmul_rn(a, u)));
             }
-            st_s<MIS>(p.x + base + (r0 + k) * kRowElems + 4 * lane, s, xn);
+            float* dst = p.x + base + (r0 + k) * kRowElems + 4 * lane;
+            const int nvl = PART ? lane_valid(tvalid, static_cast<uint64_t>(r0 + k) * kRowElems, lane) : 4;
+            if (!PART || nvl == 4) {
+              st_s<MIS>(dst, s, xn);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (q < nvl) dst[q] = comp(xn, q);
+            }
           }
         }
       };
+      // MIS accessors only for a layer off a 16-B boundary (they assume s != 0)
       if constexpr (MISK) {
-        if (s != 0) rows(Mis<true>{});
-        else rows(Mis<false>{});
+        if (s != 0) {
+          if (part) rows(Mis<true>{}, Mis<true>{});
+          else rows(Mis<true>{}, Mis<false>{});
+        } else {
+          if (part) rows(Mis<false>{}, Mis<true>{});
+          else rows(Mis<false>{}, Mis<false>{});
+        }
       } else {
-        rows(Mis<false>{});
+        if (part) rows(Mis<false>{}, Mis<true>{});
+        else rows(Mis<false>{}, Mis<false>{});
       }
       continue;
     }
@@ -1661,12 +1715,18 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
     const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
     const int s = static_cast<int>(lo & 3u);
     double ax = 0.0, au = 0.0, av = 0.0, am = 0.0;
-    if ((MISK || s == 0) && static_cast<uint64_t>(t + 1) * kTile <= len) {
-      // Fast path: full tile, 4 rows per batch, loads issued first.
-      auto rows = [&](auto mis) {
+    const uint64_t tvalid = len - static_cast<uint64_t>(t) * kTile < kTile ? len - static_cast<uint64_t>(t) * kTile
+                                                                          : static_cast<uint64_t>(kTile);
+    if (MISK || s == 0) {
+      // Fast path: 4 rows per batch, loads issued first; a partial last tile
+      // skips the rows past the layer end and masks its last row.
+      const bool part = tvalid < static_cast<uint64_t>(kTile);
+      const int rows_valid = static_cast<int>((tvalid + kRowElems - 1) / kRowElems);
+      auto rows = [&](auto mis, auto partial) {
         constexpr bool MIS = decltype(mis)::value;
+        constexpr bool PART = decltype(partial)::value;
         constexpr int R = 4;
-        for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        for (int r0 = 0; r0 < (PART ? rows_valid : kRowsPerTile); r0 += R) {
           float4 g[R], m[R], v[R], x[R];
 #pragma unroll
           for (int k = 0; k < R; ++k) {
@@ -1678,9 +1738,10 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
           }
 #pragma unroll
           for (int k = 0; k < R; ++k) {
+            const int nvl = PART ? lane_valid(tvalid, static_cast<uint64_t>(r0 + k) * kRowElems, lane) : 4;
             if (p.err && !(isfinite(g[k].x) && isfinite(g[k].y) && isfinite(g[k].z) && isfinite(g[k].w))) {
               for (int q = 0; q < 4; ++q)
-                if (!isfinite(comp(g[k], q)))
+                if ((!PART || q < nvl) && !isfinite(comp(g[k], q)))
                   flag(p.err, kErrGrad, (static_cast<unsigned long long>(p.worker_base) << 40) |
                                             (base + (r0 + k) * kRowElems + 4 * lane + q));
             }
@@ -1695,23 +1756,37 @@ __global__ void __launch_bounds__(kBlock) kw1_warmup_a(const W1Params p) {
               set_comp(vn, q, vq);
               float u = __fdiv_rn(mq, __fadd_rn(__fsqrt_rn(vq), p.eta));
               if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
-              const double xd = comp(x[k], q), ud = u, vd = vq;
-              ax += xd * xd;
-              au += ud * ud;
-              av += vd * vd;
-              am += fabs(static_cast<double>(mq));
+              if (!PART || q < nvl) {
+                const double xd = comp(x[k], q), ud = u, vd = vq;
+                ax += xd * xd;
+                au += ud * ud;
+                av += vd * vd;
+                am += fabs(static_cast<double>(mq));
+              }
             }
             const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
-            st_s<MIS>(p.m + o, s, mn);
-            st_s<MIS>(p.v + o, s, vn);
+            if (!PART || nvl == 4) {
+              st_s<MIS>(p.m + o, s, mn);
+              st_s<MIS>(p.v + o, s, vn);
+            } else {
+              st_first(p.m + o, mn, nvl);
+              st_first(p.v + o, vn, nvl);
+            }
           }
         }
       };
+      // MIS accessors only for a layer off a 16-B boundary (they assume s != 0)
       if constexpr (MISK) {
-        if (s != 0) rows(Mis<true>{});
-        else rows(Mis<false>{});
+        if (s != 0) {
+          if (part) rows(Mis<true>{}, Mis<true>{});
+          else rows(Mis<true>{}, Mis<false>{});
+        } else {
+          if (part) rows(Mis<false>{}, Mis<true>{});
+          else rows(Mis<false>{}, Mis<false>{});
+        }
       } else {
-        rows(Mis<false>{});
+        if (part) rows(Mis<false>{}, Mis<true>{});
+        else rows(Mis<false>{}, Mis<false>{});
       }
     } else
     for (int r = 0; r < kRowsPerTile; ++r) {
@@ -1855,11 +1930,18 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
     const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
     const int s = static_cast<int>(lo & 3u);
     const float a = __ldg(p.coef_x + l);
-    if ((MISK || s == 0) && static_cast<uint64_t>(t + 1) * kTile <= len) {
-      auto rows = [&](auto mis) {
+    const uint64_t tvalid = len - static_cast<uint64_t>(t) * kTile < kTile ? len - static_cast<uint64_t>(t) * kTile
+                                                                          : static_cast<uint64_t>(kTile);
+    if (MISK || s == 0) {
+      // Batched rows; a partial last tile skips the rows past the layer end
+      // and masks its last row.
+      const bool part = tvalid < static_cast<uint64_t>(kTile);
+      const int rows_valid = static_cast<int>((tvalid + kRowElems - 1) / kRowElems);
+      auto rows = [&](auto mis, auto partial) {
         constexpr bool MIS = decltype(mis)::value;
+        constexpr bool PART = decltype(partial)::value;
         constexpr int R = 4;
-        for (int r0 = 0; r0 < kRowsPerTile; r0 += R) {
+        for (int r0 = 0; r0 < (PART ? rows_valid : kRowsPerTile); r0 += R) {
           float4 m[R], v[R], x[R];
 #pragma unroll
           for (int k = 0; k < R; ++k) {
@@ -1878,16 +1960,29 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
               set_comp(xn, q, __fadd_rn(comp(x[k], q), __fmul_rn(a, u)));
             }
             const uint64_t o = base + (r0 + k) * kRowElems + 4 * lane;
-            st_s<MIS>(p.x + o, s, xn);
-            if (p.finalize) st_s<MIS>(p.vf + o, s, v[k]);  // optimizers.cpp:205
+            const int nvl = PART ? lane_valid(tvalid, static_cast<uint64_t>(r0 + k) * kRowElems, lane) : 4;
+            if (!PART || nvl == 4) {
+              st_s<MIS>(p.x + o, s, xn);
+              if (p.finalize) st_s<MIS>(p.vf + o, s, v[k]);  // optimizers.cpp:205
+            } else {
+              st_first(p.x + o, xn, nvl);
+              if (p.finalize) st_first(p.vf + o, v[k], nvl);
+            }
           }
         }
       };
+      // MIS accessors only for a layer off a 16-B boundary (they assume s != 0)
       if constexpr (MISK) {
-        if (s != 0) rows(Mis<true>{});
-        else rows(Mis<false>{});
+        if (s != 0) {
+          if (part) rows(Mis<true>{}, Mis<true>{});
+          else rows(Mis<true>{}, Mis<false>{});
+        } else {
+          if (part) rows(Mis<false>{}, Mis<true>{});
+          else rows(Mis<false>{}, Mis<false>{});
+        }
       } else {
-        rows(Mis<false>{});
+        if (part) rows(Mis<false>{}, Mis<true>{});
+        else rows(Mis<false>{}, Mis<false>{});
       }
       continue;
     }
