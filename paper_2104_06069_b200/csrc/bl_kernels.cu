@@ -2565,12 +2565,38 @@ __device__ __forceinline__ void k3_cta_tile_ll(const SmallParams& sp, long long 
     for (int i = 0; i < kMaxN; ++i)
       lv[k][i] = i < n ? ld_ll(inw + i * p.slot + 4 * (r0 + k) + (lane >> 3)) : make_uint2(0u, sp.ep32);
   }
+  if (sp.ts && blockIdx.x == 0 && threadIdx.x == 0) sp.ts[9] = now_ns() + 0ull * lv[0][0].y;
+  // Words still in flight are re-polled together, one round trip per sweep
+  // (polling them one after another cost a round trip each).
+  {
+    unsigned long long t0 = 0;
+    for (int sweep = 0;; ++sweep) {
+      bool stale = false;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int i = 0; i < kMaxN; ++i) stale |= lv[k][i].y != sp.ep32;
+      if (!stale) break;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int i = 0; i < kMaxN; ++i)
+          if (lv[k][i].y != sp.ep32) lv[k][i] = ld_ll(inw + i * p.slot + 4 * (r0 + k) + (lane >> 3));
+      if ((sweep & 63) == 63) {
+        if (t0 == 0) t0 = now_ns();
+        if (gate_closed(sp.err) || now_ns() - t0 > wait_bound(sp.err)) {
+          close_gate(sp.err, kGateMidStep);
+          ok = false;
+          break;
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int k = 0; k < R; ++k)
 #pragma unroll
-    for (int i = 0; i < kMaxN; ++i)
-      nb[k][i] = lv[k][i].y == sp.ep32 ? lv[k][i].x
-                                       : ll_get(inw + i * p.slot + 4 * (r0 + k) + (lane >> 3), sp.ep32, sp.err, ok);
+    for (int i = 0; i < kMaxN; ++i) nb[k][i] = lv[k][i].x;
+  if (sp.ts && blockIdx.x == 0 && threadIdx.x == 0) sp.ts[10] = now_ns() + 0ull * nb[R - 1][0];
   float cm = 0.0f;
 #pragma unroll
   for (int k = 0; k < R; ++k) {
@@ -2631,11 +2657,13 @@ __device__ __forceinline__ void k3_cta_tile_ll(const SmallParams& sp, long long 
       const float m = warp_max(lane < kWarpsPerBlock ? s_cm[lane] : 0.0f);
       if (lane == 0) p.cmax[t] = m;
     }
+    if (sp.ts && blockIdx.x == 0 && threadIdx.x == 0) sp.ts[11] = now_ns();
     const uint4 v = tile_words(sw, lane);
     reinterpret_cast<uint4*>(p.res_cur + static_cast<size_t>(j) * p.slot + (i0 >> 5))[lane] = v;
     for (int q = 0; q < n; ++q) st_ll4(sp.ll_res[q] + sp.ll_off + (i0 >> 5) + 4 * lane, v, sp.ep32);
   }
   __syncthreads();
+  if (sp.ts && blockIdx.x == 0 && threadIdx.x == 0) sp.ts[12] = now_ns();
 }
 
 // True in every thread of the CTA that arrives last at counter `c` (after

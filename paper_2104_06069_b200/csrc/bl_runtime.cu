@@ -260,6 +260,7 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
     // stderr after the call -- a latency-analysis aid, synchronizes the stream.
     static const bool ts_on = std::getenv("BL_SMALL_TS") != nullptr;
     if (ts_on && !small_ts) small_ts = reinterpret_cast<unsigned long long*>(dalloc<double>(16));
+    if (ts_on) cuda_check(cudaMemsetAsync(small_ts, 0, 16 * 8, stream), "ts reset");
     sp.ts = ts_on ? small_ts : nullptr;
     begin(KC_SMALL, &a);
     const int r = launch_small_collective(sp, k1_mode, stream);
@@ -267,12 +268,14 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
                                     cudaGetErrorString(static_cast<cudaError_t>(-r)));
     end(KC_SMALL, a, r);
     if (ts_on) {
-      unsigned long long h[9];
+      unsigned long long h[13];
       cuda_check(cudaMemcpyAsync(h, small_ts, sizeof h, cudaMemcpyDeviceToHost, stream), "ts");
       cuda_check(cudaStreamSynchronize(stream), "ts");
-      std::fprintf(stderr, "small_ts rank %d tiles %lld:", rank, static_cast<long long>(n) * tpc);
-      for (int k = 1; k < 9; ++k) std::fprintf(stderr, " %.2f", (h[k] - h[0]) * 1e-3);
-      std::fprintf(stderr, "\n");
+      char line[256];
+      int len = std::snprintf(line, sizeof line, "small_ts rank %d tiles %lld:", rank, static_cast<long long>(n) * tpc);
+      for (int k = 1; k < 13; ++k)
+        len += std::snprintf(line + len, sizeof line - len, " %.2f", h[k] ? (h[k] - h[0]) * 1e-3 : -1.0);
+      std::fprintf(stderr, "%s\n", line);  // one write per line (ranks share stderr)
     }
     finish_compressed(es_host, es_dev);
     return dec_out != nullptr;
