@@ -1554,7 +1554,8 @@ __global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
     } else if (p.mode == 1) {
       c = p.c_avg[l];  // optimizers.cpp:301-303
     }
-    p.coef_x[l] = static_cast<float>(-p.lr * c);
+    const double lr = p.lr_dev ? *p.lr_dev : p.lr;
+    p.coef_x[l] = static_cast<float>(-lr * c);
     p.trace[l] = c;
     p.trace[L + l] = r;
     p.trace[2 * L + l] = sqrt(s);

@@ -179,6 +179,7 @@ struct EpiParams {
   float* es_next;
   unsigned int* counter;
   double lr, r_thr, r_min, r_max, floor_;
+  const double* lr_dev;  // graph replay: the step's lr is read here (nullptr: `lr`)
   int scaled_ef;
   int mode;  // 0 onebit_lamb (ratio rule), 1 lamb_basic_1bit (c = c_avg), 2 onebit_adam (c = 1)
 };

@@ -1196,6 +1196,7 @@ void bl_optimizer::compressed_step(double lr, const float* stage_host) {
   ep.es_next = es;
   ep.counter = counter;
   ep.lr = lr;
+  ep.lr_dev = capturing ? lr_dev : nullptr;  // a captured step reads the lr staged before each replay
   ep.r_thr = hp.r_threshold;
   ep.r_min = hp.r_min;
   ep.r_max = hp.r_max;
@@ -1269,7 +1270,8 @@ void bl_optimizer::step(const float* const* grads, int n_grads, uint64_t t, doub
       cl->copy_inputs(grads, n_grads, d, memory);
     }
     cl->begin_step(this, t, true, strict);
-    compressed_step(lr, stage);
+    if (stage == nullptr && graphable()) compressed_step_graph(lr);
+    else compressed_step(lr, stage);
     compressed = true;
   }
   cl->pending_step = t;
@@ -1291,6 +1293,65 @@ void bl_optimizer::step(const float* const* grads, int n_grads, uint64_t t, doub
     }
     tr->compressed = compressed ? 1 : 0;
   }
+}
+
+// Steady state only: the momentum is encoded by the packets (K1 mode 2, K5
+// MPREV 1), no host-staged gradient, no per-collective host work (verify,
+// stats, profiling), no peer flags (their epochs are kernel arguments).
+bool bl_optimizer::graphable() const {
+  static const bool off = [] {
+    const char* e = std::getenv("BL_GRAPH");
+    return e && e[0] == '0';
+  }();
+  return !off && variant == BL_ONEBIT_LAMB && !m_valid && !mprev_separate && cl->calls == my_calls &&
+         cl->cfg.compressor == BL_COMPRESSOR_ONEBIT && !cl->cfg.verify_compensation &&
+         !cl->cfg.endpoint_stats && !cl->profiling && (cl->mode == BL_MODE_SIM || cl->n == 1) &&
+         std::getenv("BL_STATIC_TILES") == nullptr;
+}
+
+void bl_optimizer::compressed_step_graph(double lr) {
+  if (!lr_dev) {
+    lr_dev = dalloc<double>(1);
+    cuda_check(cudaMallocHost(&lr_host, sizeof(double)), "cudaMallocHost");
+  }
+  const int par = cl->cur();
+  if (!graph[par]) {  // capture this parity's step once (its kernel arguments depend only on the parity)
+    cudaGraph_t g = nullptr;
+    const uint64_t calls0 = cl->calls, launches0 = cl->launches;
+    const bl_volume_ledger led0 = cl->ledger;
+    cuda_check(cudaStreamBeginCapture(cl->stream, cudaStreamCaptureModeThreadLocal), "capture begin");
+    capturing = true;
+    try {
+      compressed_step(lr, nullptr);
+    } catch (...) {
+      capturing = false;
+      cudaStreamEndCapture(cl->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    capturing = false;
+    cuda_check(cudaStreamEndCapture(cl->stream, &g), "capture end");
+    cuda_check(cudaGraphInstantiate(&graph[par], g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+    graph_kernels[par] = cl->launches - launches0;
+    // capture enqueued nothing: undo the host bookkeeping of the captured step
+    cl->calls = calls0;
+    cl->launches = launches0;
+    cl->ledger = led0;
+    m_valid = false;
+    my_calls = calls0;
+  }
+  *lr_host = lr;
+  cuda_check(cudaMemcpyAsync(lr_dev, lr_host, sizeof(double), cudaMemcpyHostToDevice, cl->stream), "lr");
+  cuda_check(cudaGraphLaunch(graph[par], cl->stream), "graph launch");
+  // the host side of compressed_step
+  cl->calls += 1;
+  cl->last_identity = false;
+  cl->ledger_compressed();
+  cl->launches += graph_kernels[par];
+  m_valid = false;
+  mprev_separate = false;
+  my_calls = cl->calls;
 }
 
 void bl_optimizer::materialize_m(float* dst) {
@@ -2007,9 +2068,12 @@ void bl_optimizer_destroy(bl_optimizer* o) {
                   o->mprev, o->c_avg, o->r_prev, o->coeff, o->mag, o->A, o->B, o->invc, o->coef_x,
                   o->trace, o->cmean, o->es, o->counter, o->tile_sums, o->tile_max,
                   o->k1_tile_layer, o->k1_slow, o->k1_order, o->tile_order,
-                  o->w1_order, o->w2_order, o->lw_order};
+                  o->w1_order, o->w2_order, o->lw_order, o->lr_dev};
   for (void* p : bufs)
     if (p) cudaFree(p);
+  for (auto& gx : o->graph)
+    if (gx) cudaGraphExecDestroy(gx);
+  if (o->lr_host) cudaFreeHost(o->lr_host);
   delete o;
 }
 

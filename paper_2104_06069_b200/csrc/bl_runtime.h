@@ -272,5 +272,15 @@ struct bl_optimizer {
   void warmup_kernels(double lr, bool track, bool finalize, bool adam, int pieces, unsigned long long ep);
   std::vector<int> lt_start_h;  // host copy of layer_tile_start
   void compressed_step(double lr, const float* stage_host);
+  // CUDA-graph replay of the steady-state compression step (SIM mode or one
+  // rank; BL_GRAPH=0 disables): one captured graph per ping-pong parity, the
+  // step's lr staged into a device word before each launch.
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  uint64_t graph_kernels[2] = {0, 0};
+  double* lr_dev = nullptr;
+  double* lr_host = nullptr;  // pinned
+  bool capturing = false;
+  bool graphable() const;
+  void compressed_step_graph(double lr);
   void materialize_m(float* dst);
 };
