@@ -9,8 +9,6 @@ from __future__ import annotations
 
 import os
 
-import numpy as np
-
 
 def env_rank() -> tuple[int, int, int]:
     """(rank, world, local_rank) from the torchrun environment."""
@@ -68,7 +66,3 @@ def chunk_bounds(dim: int, world: int, rank: int) -> tuple[int, int]:
 def packet_bytes(chunk: int) -> int:
     """serialize() size of one chunk message (compression.cpp:91-99)."""
     return (chunk + 7) // 8 + 4
-
-
-def split_packets(blob: np.ndarray, world: int) -> list[np.ndarray]:
-    return list(blob.reshape(world, -1))
