@@ -2863,21 +2863,33 @@ __global__ void __launch_bounds__(kBlock) k_error_stats_tiles(
   }
 }
 
+// EndpointStats of one endpoint (comm_sim.cpp:108-118, 175-180), updated on
+// the device: ||delta||_2 (canonical combine of the tile partials), max|delta|,
+// max|corrected| (the compressing kernel's per-tile maxima) and the running
+// maxima.  st = {delta_l2, delta_linf, corrected_linf, max_delta_linf,
+// max_corrected_linf}; read by the host only when queried.
 __global__ void __launch_bounds__(1024) k_error_stats_final(const double* part, const float* pmax,
-                                                            int tiles, double* out) {
+                                                            int tiles, const float* cmax, int cmax_n,
+                                                            double* st) {
   __shared__ double shd[32];
   __shared__ float shf[32];
   double s = 0.0;
-  float mx = 0.0f;
+  float mx = 0.0f, cm = 0.0f;
   for (int t = threadIdx.x; t < tiles; t += 1024) {
     s += part[t];
     mx = mx < pmax[t] ? pmax[t] : mx;
   }
+  for (int t = threadIdx.x; t < cmax_n; t += 1024) cm = cm < cmax[t] ? cmax[t] : cm;
   s = block1024_sum(s, shd);
   mx = block1024_max(mx, shf);
+  cm = block1024_max(cm, shf);
   if (threadIdx.x == 0) {
-    out[0] = s;
-    out[1] = mx;
+    const double linf = mx, cinf = cm;
+    st[0] = sqrt(s);
+    st[1] = linf;
+    st[2] = cinf;
+    st[3] = st[3] < linf ? linf : st[3];
+    st[4] = st[4] < cinf ? cinf : st[4];
   }
 }
 
@@ -3308,11 +3320,11 @@ int launch_materialize_m(const uint32_t* res, int n, uint64_t c, uint64_t slot, 
 
 int launch_error_stats(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot,
                        uint64_t W, uint64_t c, uint64_t len, double* scratch, int scratch_tiles,
-                       float* scratch_max, double* out, cudaStream_t s) {
+                       float* scratch_max, const float* cmax, int cmax_n, double* st, cudaStream_t s) {
   const int g = scratch_tiles / kWarpsPerBlock + 1;
   k_error_stats_tiles<<<g < 148 * 8 ? g : 148 * 8, kBlock, 0, s>>>(
       raw, c_pad, pk, slot, W, c, len, scratch, scratch_max, scratch_tiles);
-  k_error_stats_final<<<1, 1024, 0, s>>>(scratch, scratch_max, scratch_tiles, out);
+  k_error_stats_final<<<1, 1024, 0, s>>>(scratch, scratch_max, scratch_tiles, cmax, cmax_n, st);
   return 2;
 }
 

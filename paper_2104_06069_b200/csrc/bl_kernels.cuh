@@ -339,11 +339,13 @@ int launch_materialize_error(const float* raw, uint64_t c_pad, const uint32_t* p
 int launch_materialize_m(const uint32_t* res, int n, uint64_t c, uint64_t slot, uint64_t W,
                          const uint64_t* off, int L, const float* invc, uint64_t d, float* out,
                          cudaStream_t s);
-// Endpoint statistics (comm_sim.cpp:108-118): out[0] = sum delta^2 (tile-tree
-// over the flat residual), out[1] = max|delta|.
+// Endpoint statistics (comm_sim.cpp:108-118) of one endpoint, updated in the
+// device record st[5] = {||delta||_2 (tile-tree over the flat residual),
+// max|delta|, max|corrected| (from cmax[cmax_n]), running max|delta|,
+// running max|corrected|} -- no host round trip.
 int launch_error_stats(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t slot,
                        uint64_t W, uint64_t c, uint64_t len, double* scratch, int scratch_tiles,
-                       float* scratch_max, double* out, cudaStream_t s);
+                       float* scratch_max, const float* cmax, int cmax_n, double* st, cudaStream_t s);
 int launch_set_float(float* p, float v, cudaStream_t s);
 // verify_compensation (comm_sim.cpp:83-106) for es == 1: for every element of
 // `len` flat (chunked) positions, corrected (= raw) against decompressed +

@@ -668,53 +668,26 @@ void bl_cluster::verify_last() {
   checks += static_cast<uint64_t>(nw) * n + static_cast<uint64_t>(ns);
 }
 
-void bl_cluster::refresh_stats() {  // comm_sim.cpp:108-118, 175-180
-  cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+void bl_cluster::refresh_stats() {  // comm_sim.cpp:108-118, 175-180 (device records, no sync)
   const int latest = static_cast<int>((calls + 1u) & 1u);
-  auto update = [](bl_endpoint_stats& s, double l2, double linf, double cinf) {
-    s.delta_l2 = l2;
-    s.delta_linf = linf;
-    s.corrected_linf = cinf;
-    s.max_delta_linf = std::max(s.max_delta_linf, linf);
-    s.max_corrected_linf = std::max(s.max_corrected_linf, cinf);
-  };
-  std::vector<float> cm(static_cast<size_t>(std::max(nw * n, ns)) * tpc);
-  double host[2];
+  cudaEvent_t a;
   for (int w = 0; w < nw; ++w) {
-    cudaEvent_t a;
+    const int gw = mode == BL_MODE_SIM ? w : rank;
     begin(KC_STATS, &a);
     end(KC_STATS, a,
         launch_error_stats(werr + static_cast<size_t>(w) * n * c_pad, c_pad,
-                           wpk[latest] + static_cast<size_t>(w) * n * slot, slot, W, c, P,
-                           stat_part, stat_tiles, stat_max, stat_out, stream));
-    cuda_check(cudaMemcpyAsync(host, stat_out, sizeof host, cudaMemcpyDeviceToHost, stream), "stats");
-    cuda_check(cudaMemcpyAsync(cm.data(), wcmax + static_cast<size_t>(w) * n * tpc,
-                               static_cast<size_t>(n) * tpc * sizeof(float), cudaMemcpyDeviceToHost,
-                               stream),
-               "stats");
-    cuda_check(cudaStreamSynchronize(stream), "stats sync");
-    float cmax = 0.f;
-    for (int k = 0; k < n * tpc; ++k) cmax = cmax < cm[k] ? cm[k] : cmax;
-    const int gw = mode == BL_MODE_SIM ? w : rank;
-    update(stats[gw], std::sqrt(host[0]), host[1], cmax);
+                           wpk[latest] + static_cast<size_t>(w) * n * slot, slot, W, c, P, stat_part,
+                           stat_tiles, stat_max, wcmax + static_cast<size_t>(w) * n * tpc, n * tpc,
+                           stats_dev + 5 * static_cast<size_t>(gw), stream));
   }
-  for (int s = 0; s < ns; ++s) {
-    const int j = mode == BL_MODE_SIM ? s : rank;
-    cudaEvent_t a;
+  for (int sv = 0; sv < ns; ++sv) {
+    const int j = mode == BL_MODE_SIM ? sv : rank;
     begin(KC_STATS, &a);
     end(KC_STATS, a,
-        launch_error_stats(serr + static_cast<size_t>(s) * c_pad, c_pad,
-                           res[latest] + static_cast<size_t>(j) * slot, slot, W, c, c, stat_part,
-                           stat_tiles, stat_max, stat_out, stream));
-    cuda_check(cudaMemcpyAsync(host, stat_out, sizeof host, cudaMemcpyDeviceToHost, stream), "stats");
-    cuda_check(cudaMemcpyAsync(cm.data(), scmax + static_cast<size_t>(s) * tpc,
-                               static_cast<size_t>(tpc) * sizeof(float), cudaMemcpyDeviceToHost,
-                               stream),
-               "stats");
-    cuda_check(cudaStreamSynchronize(stream), "stats sync");
-    float cmax = 0.f;
-    for (int k = 0; k < tpc; ++k) cmax = cmax < cm[k] ? cm[k] : cmax;
-    update(stats[n + j], std::sqrt(host[0]), host[1], cmax);
+        launch_error_stats(serr + static_cast<size_t>(sv) * c_pad, c_pad,
+                           res[latest] + static_cast<size_t>(j) * slot, slot, W, c, c, stat_part, stat_tiles,
+                           stat_max, scmax + static_cast<size_t>(sv) * tpc, tpc,
+                           stats_dev + 5 * static_cast<size_t>(n + j), stream));
   }
 }
 
@@ -1569,9 +1542,8 @@ bl_status bl_cluster_create(const bl_cluster_config* cfg, bl_cluster** out) {
         c->stat_tiles = static_cast<int>((c->P + kTile - 1) / kTile);
         c->stat_part = dalloc<double>(c->stat_tiles);
         c->stat_max = dalloc<float>(c->stat_tiles);
-        c->stat_out = dalloc<double>(2);
+        c->stats_dev = dalloc<double>(5 * 2 * static_cast<size_t>(c->n));
       }
-      c->stats.assign(2 * n, bl_endpoint_stats{});
       {  // API-mode K1 boundary tiles: not full, or reaching into the padding
         std::vector<int> slow;
         for (int j = 0; j < c->n; ++j)
@@ -1615,7 +1587,7 @@ void bl_cluster_destroy(bl_cluster* c) {
   void* bufs[] = {c->in,        c->werr,       c->wpk[0],          c->wpk[1],    c->rpk,
                   c->serr,      c->res_base,   c->wpart,           c->spart,     c->wcmax,
                   c->scmax,     c->out,        c->lrecv,           c->err,       c->stat_part,
-                  c->stat_max,  c->stat_out,   c->rx,              c->flags,     c->d_peer_rx,
+                  c->stat_max,  c->stats_dev,   c->rx,              c->flags,     c->d_peer_rx,
                   c->d_peer_res, c->d_peer_flags, c->d_peer_in, c->d_peer_out, c->d_peer_err,
                   c->lossless_done, c->small_bar, c->k1_slow, c->k1_order, c->tile_ctr,
                   c->piece_done,    c->gate_status, c->ll_rx, c->ll_res, c->d_peer_llrx,
@@ -1824,7 +1796,12 @@ bl_status bl_cluster_ledger(const bl_cluster* c, bl_volume_ledger* outp) {
 bl_status bl_cluster_stats(bl_cluster* c, bl_endpoint_stats* outp) {
   return guarded([&] {
     if (!c->cfg.endpoint_stats) fail(BL_ERR_LOGIC, "endpoint statistics are disabled in the config");
-    for (size_t k = 0; k < c->stats.size(); ++k) outp[k] = c->stats[k];
+    DeviceGuard g(c->device);
+    c->sync_and_check(nullptr);
+    static_assert(sizeof(bl_endpoint_stats) == 5 * sizeof(double), "EndpointStats layout");
+    cuda_check(cudaMemcpy(outp, c->stats_dev, 2 * static_cast<size_t>(c->n) * sizeof(bl_endpoint_stats),
+                          cudaMemcpyDeviceToHost),
+               "stats");
   });
 }
 

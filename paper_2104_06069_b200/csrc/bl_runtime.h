@@ -82,7 +82,7 @@ struct bl_cluster {
   unsigned long long* err = nullptr;  // [kErrSlots]
   double* stat_part = nullptr;  // stats scratch
   float* stat_max = nullptr;
-  double* stat_out = nullptr;   // [2]
+  double* stats_dev = nullptr;  // [2n][5] EndpointStats records (workers, then servers)
   int stat_tiles = 0;
 
   // Fused NVLink exchange (BL_TRANSPORT_P2P): CUDA-IPC-mapped peer buffers.
@@ -142,7 +142,6 @@ struct bl_cluster {
   uint64_t calls = 0;           // compressed collectives run (ping-pong index)
   bool last_identity = false;
   bl_volume_ledger ledger{};
-  std::vector<bl_endpoint_stats> stats;  // 2n (local endpoints refreshed)
   uint64_t launches = 0;
   bool profiling = false;
   struct Ev {
