@@ -277,3 +277,28 @@ def test_apply_remove_scaling(bl):
     _same(bl.remove_scaling(bl.apply_scaling(x, sizes, c2), sizes, c2), x, "round trip")
     with pytest.raises(bl.DimensionError):
         bl.apply_scaling(x, sizes, coeff[:2])
+
+
+def test_graph_replay_follows_the_lr_schedule(bl):
+    """The steady-state compression step is replayed from a captured CUDA
+    graph; its lr is staged into device memory before each replay.  A
+    per-step lr (schedule.cpp-style decay) must still give the oracle's
+    trajectory bit for bit, at n = 1 and with 4 simulated ranks."""
+    for n in (1, 4):
+        d = sum(SIZES)
+        steps, warm = 12, 3
+        cl = bl.SimCluster(n, d)
+        opt = bl.Optimizer("onebit_lamb", SIZES, bl.HyperParams(total_steps=steps, warmup_steps=warm), cl)
+        ocl = O.Cluster("f32", n, d)
+        oopt = O.Optimizer("f32", "onebit_lamb", SIZES, O.HyperParams(total_steps=steps, warmup_steps=warm))
+        rng = np.random.default_rng(77 + n)
+        x0 = (rng.standard_normal(d) * 0.02).astype(np.float32)
+        opt.set("x", x0)
+        oopt.set("x", x0)
+        for t in range(steps):
+            lr = 1e-3 * (0.7 ** t)
+            g = (rng.standard_normal((n, d)) * 1e-3).astype(np.float32)
+            tr = opt.step(g, t, lr)
+            otr = oopt.step(g, t, lr, ocl)
+            _same(tr.c, otr["c"], f"c t={t} n={n}")
+        _same(opt.get("x"), oopt.get("x"), f"x n={n}")
