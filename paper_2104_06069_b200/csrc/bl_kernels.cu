@@ -773,35 +773,53 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
   }
   __syncwarp();
 
+  // Tile index -> (worker, chunk, tile-in-chunk) in 32-bit arithmetic (the
+  // index space is below 2^31): 64-bit divisions here cost ~50 issued
+  // instructions per row when they ran per stage (ncu: 200 per row).
+  const unsigned int per_w32 = static_cast<unsigned int>(per_w), tpc32 = static_cast<unsigned int>(p.tpc);
+  auto split = [&](long long tile, int& w, int& j, int& t) {
+    const unsigned int u = static_cast<unsigned int>(tile);
+    w = static_cast<int>(u / per_w32);
+    const unsigned int rem = u - static_cast<unsigned int>(w) * per_w32;
+    j = static_cast<int>(rem / tpc32);
+    t = static_cast<int>(rem - static_cast<unsigned int>(j) * tpc32);
+  };
   auto is_fast = [&](long long tile) {
-    const int w = static_cast<int>(tile / per_w);
-    const long long rem = tile - w * per_w;
-    const int j = static_cast<int>(rem / p.tpc);
-    return k1_fast_layer<MODE>(p, j, static_cast<int>(rem - static_cast<long long>(j) * p.tpc)) >= 0;
+    int w, j, t;
+    split(tile, w, j, t);
+    return k1_fast_layer<MODE>(p, j, t) >= 0;
   };
   auto next_fast = [&](long long tile) {
     while (tile < total && !is_fast(tile)) tile += nwarps;
     return tile;
   };
-  // Producer: lane 0 issues the copies of batch (tile, r0) into `stage`.
-  auto issue = [&](int stage, long long tile, int r0) {
+  // Producer state of the tile being issued -- its source rows, formed once
+  // per tile (not per stage) by lane 0 and kept in shared memory (registers
+  // are the consumer's).
+  __shared__ const void* s_src[kBulkWarps][4];
+  auto bind = [&](long long tile) {
     if (tile >= total || lane != 0) return;
-    const int w = static_cast<int>(tile / per_w);
-    const long long rem = tile - w * per_w;
-    const int j = static_cast<int>(rem / p.tpc);
-    const int t = static_cast<int>(rem - static_cast<long long>(j) * p.tpc);
+    int w, j, t;
+    split(tile, w, j, t);
     const uint64_t i0 = static_cast<uint64_t>(t) * kTile, kc = static_cast<uint64_t>(j) * p.c;
     const size_t ep = static_cast<size_t>(w) * p.n + j;
-    const int s = static_cast<int>(kc & 3u);
+    s_src[wib][0] = p.in + static_cast<size_t>(w) * p.in_stride + kc + i0 - static_cast<int>(kc & 3u);
+    s_src[wib][1] = p.werr + ep * p.c_pad + i0;
+    s_src[wib][2] = p.pk_prev + ep * p.slot + (i0 >> 5);
+    s_src[wib][3] = p.res_prev + static_cast<size_t>(j) * p.slot + (i0 >> 5);
+  };
+  // Producer: lane 0 issues the copies of batch (bound tile, r0) into `stage`.
+  auto issue = [&](int stage, long long tile, int r0) {
+    if (tile >= total || lane != 0) return;
     unsigned char* st = wsm + stage * kBulkStage;
     unsigned long long* bar = &bars[wib][stage];
     mbar_expect_tx(bar, kBulkG + kBulkW + (MODE == 2 ? 2 : 1) * kBulkBits);
-    bulk_g2s(st, p.in + static_cast<size_t>(w) * p.in_stride + kc + i0 + r0 * kRowElems - s, kBulkG, bar);
-    bulk_g2s(st + kBulkG, p.werr + ep * p.c_pad + i0 + r0 * kRowElems, kBulkW, bar);
-    bulk_g2s(st + kBulkG + kBulkW, p.pk_prev + ep * p.slot + (i0 >> 5) + 4 * r0, kBulkBits, bar);
+    bulk_g2s(st, static_cast<const float*>(s_src[wib][0]) + r0 * kRowElems, kBulkG, bar);
+    bulk_g2s(st + kBulkG, static_cast<const float*>(s_src[wib][1]) + r0 * kRowElems, kBulkW, bar);
+    bulk_g2s(st + kBulkG + kBulkW, static_cast<const uint32_t*>(s_src[wib][2]) + 4 * r0, kBulkBits, bar);
     if (MODE == 2)
-      bulk_g2s(st + kBulkG + kBulkW + kBulkBits,
-               p.res_prev + static_cast<size_t>(j) * p.slot + (i0 >> 5) + 4 * r0, kBulkBits, bar);
+      bulk_g2s(st + kBulkG + kBulkW + kBulkBits, static_cast<const uint32_t*>(s_src[wib][3]) + 4 * r0,
+               kBulkBits, bar);
   };
 
   // Producer sequence: with a tile counter the fast tiles are taken
@@ -817,6 +835,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
     return t;
   };
   long long ptile = p.ctr ? fetch_fast(true) : next_fast(gw);
+  bind(ptile);
   int pr = 0;
   auto produce = [&](int stage) {
     if (lane == 0) {
@@ -829,6 +848,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
     if (pr == kRowsPerTile) {
       pr = 0;
       ptile = p.ctr ? fetch_fast(false) : next_fast(ptile + nwarps);
+      bind(ptile);
     }
   };
   for (int s = 0; s < kBulkStages; ++s) produce(s);
@@ -867,10 +887,8 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
     cr = s_r0[wib][stage];
     if (ctile >= total) break;
     if (cr == 0) {
-      w = static_cast<int>(ctile / per_w);
-      const long long rem = ctile - w * per_w;
-      const int j = static_cast<int>(rem / p.tpc);
-      t = static_cast<int>(rem - static_cast<long long>(j) * p.tpc);
+      int j;
+      split(ctile, w, j, t);
       i0 = static_cast<uint64_t>(t) * kTile;
       kc = static_cast<uint64_t>(j) * p.c;
       s = static_cast<int>(kc & 3u);
