@@ -1987,6 +1987,23 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
               st_first(p.x + o, xn, nvl);
               if (p.finalize) st_first(p.vf + o, v[k], nvl);
             }
+            for (int j = 0; j < p.npush; ++j) {  // owner-sharded warmup: the allgather
+              if (!PART || nvl == 4) {
+                st_s<MIS>(p.push_x[j] + o, s, xn);
+                if (p.finalize) {
+                  st_s<MIS>(p.push_m[j] + o, s, m[k]);
+                  st_s<MIS>(p.push_v[j] + o, s, v[k]);
+                  st_s<MIS>(p.push_vf[j] + o, s, v[k]);
+                }
+              } else {
+                st_first(p.push_x[j] + o, xn, nvl);
+                if (p.finalize) {
+                  st_first(p.push_m[j] + o, m[k], nvl);
+                  st_first(p.push_v[j] + o, v[k], nvl);
+                  st_first(p.push_vf[j] + o, v[k], nvl);
+                }
+              }
+            }
           }
         }
       };
@@ -2022,8 +2039,17 @@ __global__ void __launch_bounds__(kBlock) kw2_warmup_b(const W2Params p) {
       }
       st_row4(p.x + kr, lane, s, xn, nv);
       if (p.finalize) st_row4(p.vf + kr, lane, s, v, nv);  // optimizers.cpp:205
+      for (int j = 0; j < p.npush; ++j) {  // owner-sharded warmup: the allgather
+        st_row4(p.push_x[j] + kr, lane, s, xn, nv);
+        if (p.finalize) {
+          st_row4(p.push_m[j] + kr, lane, s, m, nv);
+          st_row4(p.push_v[j] + kr, lane, s, v, nv);
+          st_row4(p.push_vf[j] + kr, lane, s, v, nv);
+        }
+      }
     }
   }
+  if (p.npush) warp_fence_system(lane);  // remote stores before the stream's signal
 }
 
 // Lossless average (comm_sim.cpp:214-222): ascending workers in fp64, * 1/n.
@@ -2133,7 +2159,11 @@ __device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint
     if (k >= end) break;
     const float4 v = make_float4(static_cast<float>(a[u][0] * inv_n), static_cast<float>(a[u][1] * inv_n),
                                  static_cast<float>(a[u][2] * inv_n), static_cast<float>(a[u][3] * inv_n));
-    for (int q = 0; q < n; ++q) *reinterpret_cast<float4*>(p.peer_out[q] + k) = v;
+    if (p.local_only) {
+      *reinterpret_cast<float4*>(p.peer_out[p.rank] + k) = v;
+    } else {
+      for (int q = 0; q < n; ++q) *reinterpret_cast<float4*>(p.peer_out[q] + k) = v;
+    }
   }
 }
 
@@ -2152,7 +2182,7 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
   if (gate_closed_call(p.err)) return;
   if (!wait_peers(p.in_flags, p.n, p.epoch, p.err)) return;  // every rank's gradient is in place
   const double inv_n = 1.0 / static_cast<double>(p.n);
-  const uint64_t lo = static_cast<uint64_t>(p.rank) * p.c, hi = lo + p.c;
+  const uint64_t lo = p.hi ? p.lo : static_cast<uint64_t>(p.rank) * p.c, hi = p.hi ? p.hi : lo + p.c;
   const uint64_t up = (lo + 3) & ~3ull, dn = hi & ~3ull;  // 16-B aligned body [a0, a1)
   const uint64_t a0 = up < hi ? up : hi;
   const uint64_t a1 = dn > a0 ? dn : a0;
@@ -2176,7 +2206,7 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
           acc += static_cast<double>(x);
         }
         const float v = static_cast<float>(acc * inv_n);
-        for (int q = 0; q < p.n; ++q) p.peer_out[q][k] = v;
+        for (int q = p.local_only ? p.rank : 0; q < (p.local_only ? p.rank + 1 : p.n); ++q) p.peer_out[q][k] = v;
       }
     }
     if (p.pieces > 0) {
@@ -2192,7 +2222,7 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
             forward_grad_error(p.err, p.peer_err, p.n);  // every rank raises (optimizers.cpp:99-117)
           }
           __threadfence_system();
-          for (int q = 0; q < p.n; ++q)
+          for (int q = p.local_only ? p.rank : 0; q < (p.local_only ? p.rank + 1 : p.n); ++q)
             st_relaxed_sys(p.peer_flags[q] + p.piece_flag_base + p.rank * p.pieces + pc, p.epoch);
         }
       }
@@ -2205,8 +2235,21 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
     __threadfence();
     forward_grad_error(p.err, p.peer_err, p.n);  // every rank raises (optimizers.cpp:99-117)
     __threadfence_system();
-    for (int q = 0; q < p.n; ++q) st_relaxed_sys(p.peer_flags[q] + p.out_flag + p.rank, p.epoch);
+    for (int q = p.local_only ? p.rank : 0; q < (p.local_only ? p.rank + 1 : p.n); ++q)
+      st_relaxed_sys(p.peer_flags[q] + p.out_flag + p.rank, p.epoch);
   }
+}
+
+template <typename T>
+__global__ void k_push_range(const T* src, T* const* dst, int ndst, uint64_t off, uint64_t count,
+                             const unsigned long long* gate) {
+  if (gate_closed_call(gate)) return;
+  const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < count; k += nth) {
+    const T w = __ldcg(src + off + k);
+    for (int j = 0; j < ndst; ++j) dst[j][off + k] = w;
+  }
+  __threadfence_system();
 }
 
 // Consumer side of the piecewise exchange: every rank's piece p delivered.
@@ -3400,7 +3443,7 @@ int launch_wait_piece(const unsigned long long* flags, int base, int n, int piec
 }
 
 int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s) {
-  const long long groups = static_cast<long long>(p.c / 4) + 1;
+  const long long groups = static_cast<long long>((p.hi ? p.hi - p.lo : p.c) / 4) + 1;
   const long long cap = p.ctas > 0 ? p.ctas : 8ll * sms;
   const int want = static_cast<int>(std::min<long long>((groups + 255) / 256, cap));  // (256-thread estimate)
   const int bt = p.block > 0 ? p.block : 256;
@@ -3410,6 +3453,23 @@ int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s) {
     case 8: k_lossless_p2p<8><<<resident(k_lossless_p2p<8>, want), bt, 0, s>>>(p); break;
     default: k_lossless_p2p<0><<<resident(k_lossless_p2p<0>, want), bt, 0, s>>>(p); break;
   }
+  return 1;
+}
+
+int launch_push_range(const float* src, float* const* dst, int ndst, uint64_t off, uint64_t count,
+                      const unsigned long long* gate, int sms, cudaStream_t s) {
+  if (count == 0 || ndst == 0) return 0;
+  const uint64_t want = (count + 255) / 256;
+  k_push_range<float><<<static_cast<int>(want < static_cast<uint64_t>(4 * sms) ? want : 4 * sms), 256, 0, s>>>(
+      src, dst, ndst, off, count, gate);
+  return 1;
+}
+int launch_push_range(const double* src, double* const* dst, int ndst, uint64_t off, uint64_t count,
+                      const unsigned long long* gate, int sms, cudaStream_t s) {
+  if (count == 0 || ndst == 0) return 0;
+  const uint64_t want = (count + 255) / 256;
+  k_push_range<double><<<static_cast<int>(want < static_cast<uint64_t>(4 * sms) ? want : 4 * sms), 256, 0, s>>>(
+      src, dst, ndst, off, count, gate);
   return 1;
 }
 

@@ -247,6 +247,10 @@ struct LosslessP2PParams {
   unsigned int* piece_done;               // [pieces] local CTA counters (self-resetting)
   int ctas;                               // grid cap (leave SM room for the consumer), 0 = full
   int block;                              // threads per CTA (0 = 256)
+  // Owner-sharded warmup: reduce [lo, hi) instead of chunk `rank` and store
+  // the average into the local output only (no allgather; hi == 0: chunk).
+  uint64_t lo, hi;
+  int local_only;
 };
 
 struct W1Params {
@@ -292,6 +296,13 @@ struct W2Params {
   const float* coef_x;
   float eta, wd;
   int finalize;
+  // Owner-sharded warmup: x (and at the freeze m, v, vf) of the owned tiles
+  // is also stored into the npush other ranks' buffers (the allgather).
+  float* const* push_x;
+  float* const* push_m;
+  float* const* push_v;
+  float* const* push_vf;
+  int npush;
 };
 
 // Step gate (start of every step / collective).  Strict mode: a non-finite
@@ -368,6 +379,13 @@ int launch_signal_peers(unsigned long long* const* peer_flags, int index, int n,
                         unsigned long long epoch, const unsigned long long* gate, cudaStream_t s);
 int launch_wait_peers(const unsigned long long* flags, int n, unsigned long long epoch,
                       unsigned long long* err, cudaStream_t s);
+// Store words [off, off + count) of src into the same range of every buffer
+// of dst[0..ndst) (peer memory), each thread fencing its remote stores; a
+// following launch_signal_peers publishes them.  4- or 8-byte words.
+int launch_push_range(const float* src, float* const* dst, int ndst, uint64_t off, uint64_t count,
+                      const unsigned long long* gate, int sms, cudaStream_t s);
+int launch_push_range(const double* src, double* const* dst, int ndst, uint64_t off, uint64_t count,
+                      const unsigned long long* gate, int sms, cudaStream_t s);
 // Strict pre-pass (optimizers.cpp:99-117, before any mutation): flags the
 // first non-finite element of the nw local gradients in kErrGrad.
 int launch_check_finite(const float* in, uint64_t stride, int nw, uint64_t d, unsigned long long* err,

@@ -442,27 +442,12 @@ void bl_cluster::finish_compressed(float es_host, const float* es_dev) {
 // Map every peer's receive buffer, result buffer and flag words into this
 // process (CUDA IPC over NVLink).  Collective: every rank takes the same
 // decision (NCCL min-reduce of the per-rank success bit).
-void bl_cluster::setup_p2p(bool required) {
-  const size_t nn = static_cast<size_t>(n);
-  rx = dalloc<uint32_t>(2 * nn * slot);
-  flags = reinterpret_cast<unsigned long long*>(
-      dalloc<double>(static_cast<size_t>(piece_flag_base()) + nn * kMaxPieces));
-  piece_done = reinterpret_cast<unsigned int*>(dalloc<float>(kMaxPieces));
-  lossless_done = reinterpret_cast<unsigned int*>(dalloc<float>(1));
-  small_bar = reinterpret_cast<unsigned int*>(dalloc<float>(2));
-  // LL buffers of the fused small collective, [2][n][slot] (word, epoch)
-  // pairs; only sized when the small path can be taken.
-  const size_t ll_words = static_cast<long long>(n) * tpc <= small_max_tiles() ? 2 * nn * slot : 1;
-  ll_rx = reinterpret_cast<uint2*>(dalloc<double>(ll_words));
-  ll_res = reinterpret_cast<uint2*>(dalloc<double>(ll_words));
-  // Buffers every peer maps: packet receive slots, result packets, flags,
-  // gradient (lossless reads), output (lossless allgather), error words,
-  // LL receive slots, LL result slots.
-  constexpr int kB = 8;
-  void* const local[kB] = {rx, res_base, flags, in, out, err, ll_rx, ll_res};
+bool bl_cluster::map_peer_buffers(const std::vector<void*>& local, std::vector<std::vector<void*>>* peer,
+                                  std::vector<void*>* opened) {
+  const size_t nn = static_cast<size_t>(n), kB = local.size();
   constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
   std::vector<uint8_t> mine(kB * kH);
-  for (int k = 0; k < kB; ++k) {
+  for (size_t k = 0; k < kB; ++k) {
     cudaIpcMemHandle_t h;
     cuda_check(cudaIpcGetMemHandle(&h, local[k]), "cudaIpcGetMemHandle");
     std::memcpy(mine.data() + k * kH, &h, kH);
@@ -477,21 +462,22 @@ void bl_cluster::setup_p2p(bool required) {
   std::vector<uint8_t> all(nn * kB * kH);
   cuda_check(cudaMemcpyAsync(all.data(), dbuf, all.size(), cudaMemcpyDeviceToHost, stream), "handles");
   cuda_check(cudaStreamSynchronize(stream), "handles sync");
-  std::vector<std::vector<void*>> peer(kB, std::vector<void*>(nn, nullptr));
+  peer->assign(kB, std::vector<void*>(nn, nullptr));
+  std::vector<void*> mapped;
   int ok = 1;
   for (int q = 0; q < n; ++q) {
-    for (int k = 0; k < kB && ok; ++k) {
+    for (size_t k = 0; k < kB && ok; ++k) {
       if (q == rank) {
-        peer[k][q] = local[k];
+        (*peer)[k][q] = local[k];
         continue;
       }
       cudaIpcMemHandle_t hq;
       std::memcpy(&hq, all.data() + (static_cast<size_t>(q) * kB + k) * kH, kH);
-      if (cudaIpcOpenMemHandle(&peer[k][q], hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      if (cudaIpcOpenMemHandle(&(*peer)[k][q], hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
         cudaGetLastError();
         ok = 0;
       } else {
-        ipc_opened.push_back(peer[k][q]);
+        mapped.push_back((*peer)[k][q]);
       }
     }
   }
@@ -502,8 +488,33 @@ void bl_cluster::setup_p2p(bool required) {
   cuda_check(cudaStreamSynchronize(stream), "ok sync");
   cudaFree(dbuf);
   if (!ok) {
-    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
-    ipc_opened.clear();
+    for (void* p : mapped) cudaIpcCloseMemHandle(p);
+    return false;
+  }
+  opened->insert(opened->end(), mapped.begin(), mapped.end());
+  return true;
+}
+
+// Map every peer's receive buffer, result buffer and flag words into this
+// process (CUDA IPC over NVLink).  Collective: every rank takes the same
+// decision (NCCL min-reduce of the per-rank success bit).
+void bl_cluster::setup_p2p(bool required) {
+  const size_t nn = static_cast<size_t>(n);
+  rx = dalloc<uint32_t>(2 * nn * slot);
+  flags = reinterpret_cast<unsigned long long*>(dalloc<double>(static_cast<size_t>(shard_flag_base()) + 2 * nn));
+  piece_done = reinterpret_cast<unsigned int*>(dalloc<float>(kMaxPieces));
+  lossless_done = reinterpret_cast<unsigned int*>(dalloc<float>(1));
+  small_bar = reinterpret_cast<unsigned int*>(dalloc<float>(2));
+  // LL buffers of the fused small collective, [2][n][slot] (word, epoch)
+  // pairs; only sized when the small path can be taken.
+  const size_t ll_words = static_cast<long long>(n) * tpc <= small_max_tiles() ? 2 * nn * slot : 1;
+  ll_rx = reinterpret_cast<uint2*>(dalloc<double>(ll_words));
+  ll_res = reinterpret_cast<uint2*>(dalloc<double>(ll_words));
+  // Buffers every peer maps: packet receive slots, result packets, flags,
+  // gradient (lossless reads), output (lossless allgather), error words,
+  // LL receive slots, LL result slots.
+  std::vector<std::vector<void*>> peer;
+  if (!map_peer_buffers({rx, res_base, flags, in, out, err, ll_rx, ll_res}, &peer, &ipc_opened)) {
     if (required) fail(BL_ERR_UNSUPPORTED, "P2P transport: a peer's memory could not be mapped");
     transport = BL_TRANSPORT_NCCL;
     return;
@@ -954,7 +965,10 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   // (float)((0.0 + g) * 1.0) is g itself: W1 reads the gradient in place and
   // only the finite check runs.
   const bool single = cl->n == 1;
-  cudaEvent_t a;
+  if (sharded_warmup()) {
+    warmup_sharded(lr, track, finalize, adam);
+    return;
+  }
   // Multi-process over NVLink: the exchange is delivered piece by piece and
   // W1 / the layer epilogue / W2 follow it (same kernels on tile and layer
   // subsets), so the NVLink transfer and the HBM-bound update overlap.
@@ -974,6 +988,155 @@ void bl_optimizer::warmup_step(uint64_t, double lr, bool track, bool finalize, b
   if (!single) cl->lossless(true);
   cl->ledger_lossless();
   warmup_kernels(lr, track, finalize, adam, 0, 0);
+}
+
+bool bl_optimizer::sharded_warmup() const {
+  if (cl->n == 1 || cl->mode != BL_MODE_NCCL || cl->transport != BL_TRANSPORT_P2P) return false;
+  if (std::getenv("BL_STATIC_TILES") != nullptr) return false;
+  const char* e = std::getenv("BL_WARMUP_SHARD");
+  return e == nullptr || std::atoi(e) != 0;
+}
+
+// Collective (every rank's first sharded warmup step): tile ownership and
+// the peer mappings of x, m, v, vf and the tile partials.
+void bl_optimizer::setup_shard() {
+  const int n = cl->n, r = cl->rank;
+  shard_t0 = static_cast<int>(static_cast<long long>(tiles) * r / n);
+  shard_t1 = static_cast<int>(static_cast<long long>(tiles) * (r + 1) / n);
+  auto tile_elem = [&](int tile) -> uint64_t {
+    if (tile >= tiles) return d;
+    const int l = static_cast<int>(std::upper_bound(lt_start_h.begin(), lt_start_h.end(), tile) -
+                                   lt_start_h.begin()) - 1;
+    return off[l] + static_cast<uint64_t>(tile - lt_start_h[l]) * kTile;
+  };
+  shard_e0 = tile_elem(shard_t0);
+  shard_e1 = tile_elem(shard_t1);
+  std::vector<int> own;
+  for (int t : tile_order_h)
+    if (t >= shard_t0 && t < shard_t1) own.push_back(t);
+  own_count = static_cast<int>(own.size());
+  own_order = reinterpret_cast<int*>(dalloc<float>(own.size()));
+  if (!own.empty())
+    cuda_check(cudaMemcpy(own_order, own.data(), own.size() * 4, cudaMemcpyHostToDevice), "own order");
+  std::vector<std::vector<void*>> peer;
+  if (!cl->map_peer_buffers({x, m, v, vf, tile_sums}, &peer, &shard_ipc))
+    fail(BL_ERR_UNSUPPORTED, "sharded warmup: a peer's optimizer state could not be mapped");
+  auto table = [&](int k) {
+    std::vector<void*> others;
+    for (int q = 0; q < n; ++q)
+      if (q != r) others.push_back(peer[k][q]);
+    void** t = reinterpret_cast<void**>(dalloc<double>(others.size()));
+    cuda_check(cudaMemcpy(t, others.data(), others.size() * sizeof(void*), cudaMemcpyHostToDevice), "tables");
+    return t;
+  };
+  push_x = reinterpret_cast<float**>(table(0));
+  push_m = reinterpret_cast<float**>(table(1));
+  push_v = reinterpret_cast<float**>(table(2));
+  push_vf = reinterpret_cast<float**>(table(3));
+  push_sums = reinterpret_cast<double**>(table(4));
+  shard_ready = true;
+}
+
+// Owner-sharded warmup step (multi-process over NVLink; optimizers.cpp:119-177,
+// 202-224 with the same per-element arithmetic and per-tile partials):
+//   reduce the owned gradient range from every rank (NVLink reads) -> W1 on
+//   the owned tiles -> tile partials to every rank -> the layer epilogue on
+//   all layers (replicated, identical inputs) -> W2 on the owned tiles,
+//   storing x into every rank -> wait until every owner delivered.
+// Per rank: the NVLink bytes of the all-reduce, a 1/n share of the HBM work.
+void bl_optimizer::warmup_sharded(double lr, bool track, bool finalize, bool adam) {
+  if (!shard_ready) setup_shard();
+  const int nn = cl->n;
+  const unsigned long long ep = ++cl->lcalls;
+  const int sbase = cl->shard_flag_base();
+  cudaEvent_t a;
+  cl->begin(KC_A2A, &a);
+  cl->end(KC_A2A, a, launch_signal_peers(cl->d_peer_flags, 2 * nn + cl->rank, nn, ep, cl->err, cl->stream));
+  LosslessP2PParams lp{};
+  lp.peer_in = cl->d_peer_in;
+  lp.peer_out = cl->d_peer_out;
+  lp.peer_err = cl->d_peer_err;
+  lp.peer_flags = cl->d_peer_flags;
+  lp.in_flags = cl->flags + 2 * nn;
+  lp.out_flag = 3 * nn;
+  lp.n = nn;
+  lp.rank = cl->rank;
+  lp.check_finite = 1;
+  lp.c = cl->c;
+  lp.d = d;
+  lp.epoch = ep;
+  lp.done = cl->lossless_done;
+  lp.err = cl->err;
+  lp.lo = shard_e0;
+  lp.hi = shard_e1;
+  lp.local_only = 1;
+  const char* be = std::getenv("BL_LOSSLESS_BLOCK");
+  lp.block = be ? std::atoi(be) : 0;
+  if (shard_e1 > shard_e0) {
+    cl->begin(KC_AVG, &a);
+    cl->end(KC_AVG, a, launch_lossless_p2p(lp, cl->sms, cl->stream));
+  }
+  cl->ledger_lossless();
+
+  // W1 / epilogue / W2 parameters of the replicated path, restricted below.
+  W1Params w1{};
+  w1.gate = cl->err;
+  w1.lt = lt();
+  w1.lt.order = own_order;
+  w1.lt.count = own_count;
+  w1.gbar = cl->out;
+  w1.m = m;
+  w1.v = v;
+  w1.x = x;
+  w1.b1 = static_cast<float>(hp.beta1);
+  w1.omb1 = static_cast<float>(1.0 - hp.beta1);
+  w1.b2 = static_cast<float>(hp.beta2);
+  w1.omb2 = static_cast<float>(1.0 - hp.beta2);
+  w1.eta = static_cast<float>(hp.eta);
+  w1.wd = static_cast<float>(hp.weight_decay);
+  w1.tile_sums = tile_sums;
+  w1.adam = adam ? 1 : 0;
+  w1.worker_base = cl->rank;
+  if (own_count) {
+    cl->begin(KC_W1, &a);
+    cl->end(KC_W1, a, launch_w1(w1, cl->grid(own_count), cl->stream));
+  }
+  cl->begin(KC_AG, &a);
+  cl->end(KC_AG, a,
+          launch_push_range(tile_sums, push_sums, nn - 1, 4ull * static_cast<uint64_t>(shard_t0),
+                            4ull * static_cast<uint64_t>(shard_t1 - shard_t0), cl->err, cl->sms, cl->stream));
+  cl->begin(KC_AG, &a);
+  cl->end(KC_AG, a, launch_signal_peers(cl->d_peer_flags, sbase + cl->rank, nn, ep, cl->err, cl->stream));
+  cl->begin(KC_AG, &a);
+  cl->end(KC_AG, a, launch_wait_peers(cl->flags + sbase, nn, ep, cl->err, cl->stream));
+  warmup_kernels(lr, track, finalize, adam, -1, ep);  // the epilogue (all layers) and W2 (owned tiles)
+  cl->begin(KC_AG, &a);
+  cl->end(KC_AG, a, launch_signal_peers(cl->d_peer_flags, sbase + nn + cl->rank, nn, ep, cl->err, cl->stream));
+  cl->begin(KC_AG, &a);
+  cl->end(KC_AG, a, launch_wait_peers(cl->flags + sbase + nn, nn, ep, cl->err, cl->stream));
+  shard_stale = !finalize;
+}
+
+// Collective: push every owner's m and v slices to every rank (a state read
+// during the multi-process warmup stage, where they are kept by their owners).
+void bl_optimizer::sync_shards() {
+  if (!shard_stale) return;
+  const int nn = cl->n;
+  const unsigned long long ep = ++cl->lcalls;
+  const int sbase = cl->shard_flag_base();
+  cudaEvent_t a;
+  for (float* const* t : {push_m, push_v}) {
+    const float* src = t == push_m ? m : v;
+    cl->begin(KC_AG, &a);
+    cl->end(KC_AG, a, launch_push_range(src, t, nn - 1, shard_e0, shard_e1 - shard_e0, cl->err, cl->sms,
+                                        cl->stream));
+  }
+  cl->begin(KC_AG, &a);
+  cl->end(KC_AG, a, launch_signal_peers(cl->d_peer_flags, sbase + cl->rank, nn, ep, cl->err, cl->stream));
+  cl->begin(KC_AG, &a);
+  cl->end(KC_AG, a, launch_wait_peers(cl->flags + sbase, nn, ep, cl->err, cl->stream));
+  cl->sync_and_check(this);
+  shard_stale = false;
 }
 
 // W1 -> layer epilogue -> W2 (optimizers.cpp:140-177, 202-224).  K > 0: per
@@ -1040,6 +1203,22 @@ void bl_optimizer::warmup_kernels(double lr, bool track, bool finalize, bool ada
   w2.eta = static_cast<float>(hp.eta);
   w2.wd = static_cast<float>(hp.weight_decay);
   w2.finalize = finalize ? 1 : 0;
+  if (K < 0) {  // owner-sharded: W1 ran on the owned tiles; epilogue, then W2 + allgather
+    cl->begin(KC_WEPI, &a);
+    cl->end(KC_WEPI, a, launch_wepilogue(we, cl->stream));
+    w2.lt.order = own_order;
+    w2.lt.count = own_count;
+    w2.push_x = push_x;
+    w2.push_m = push_m;
+    w2.push_v = push_v;
+    w2.push_vf = push_vf;
+    w2.npush = cl->n - 1;
+    if (own_count) {
+      cl->begin(KC_W2, &a);
+      cl->end(KC_W2, a, launch_w2(w2, cl->grid(own_count), cl->stream));
+    }
+    return;
+  }
   if (K == 0) {
     cl->begin(KC_W1, &a);
     cl->end(KC_W1, a, launch_w1(w1, cl->grid(tiles), cl->stream));
@@ -2048,6 +2227,10 @@ void bl_optimizer_destroy(bl_optimizer* o) {
                   o->w1_order, o->w2_order, o->lw_order, o->lr_dev};
   for (void* p : bufs)
     if (p) cudaFree(p);
+  for (void* p : o->shard_ipc) cudaIpcCloseMemHandle(p);
+  void* shard_bufs[] = {o->own_order, o->push_x, o->push_m, o->push_v, o->push_vf, o->push_sums};
+  for (void* p : shard_bufs)
+    if (p) cudaFree(p);
   for (auto& gx : o->graph)
     if (gx) cudaGraphExecDestroy(gx);
   if (o->lr_host) cudaFreeHost(o->lr_host);
@@ -2074,6 +2257,7 @@ bl_status bl_optimizer_get_state(bl_optimizer* o, int32_t which, float* host_out
     if (!o->cl) fail(BL_ERR_LOGIC, "the optimizer's cluster was destroyed");
     DeviceGuard g(o->cl->device);
     o->cl->sync_and_check(o);
+    if (which == BL_STATE_M || which == BL_STATE_V) o->sync_shards();  // collective while sharded
     const float* src = nullptr;
     switch (which) {
       case BL_STATE_X: src = o->x; break;

@@ -207,6 +207,13 @@ struct bl_cluster {
   unsigned long long lossless_pieces(bool check_finite, int pieces);
   int piece_flag_base() const { return 6 * n + 8; }
   static constexpr int kMaxPieces = 64;
+  // Owner-sharded warmup flags: [n] tile partials delivered, [n] owned x delivered.
+  int shard_flag_base() const { return piece_flag_base() + n * kMaxPieces; }
+  // Map `local` buffers of every rank into this process (CUDA IPC; collective).
+  // peer[k][q] = rank q's buffer k (own rank: local[k]); false if any peer
+  // could not be mapped on some rank (then nothing stays open).
+  bool map_peer_buffers(const std::vector<void*>& local, std::vector<std::vector<void*>>* peer,
+                        std::vector<void*>* opened);
   unsigned int* piece_done = nullptr;  // [kMaxPieces]
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -256,6 +263,23 @@ struct bl_optimizer {
   int* lw_order = nullptr;  // [L]
   std::vector<int> w1_start, w2_start, lw_start;  // [piece_k + 1]
   void build_piece_tables(int pieces);
+  // Owner-sharded warmup (multi-process over NVLink): rank r owns tiles
+  // [shard_t0, shard_t1) = elements [shard_e0, shard_e1); it reduces only the
+  // owned gradient, runs W1/W2 on the owned tiles, and stores its x (and at
+  // the freeze m, v, vf) into every peer.  m and v of the other owners' tiles
+  // are stale until the freeze or a (collective) state read.
+  bool shard_ready = false, shard_stale = false;
+  int shard_t0 = 0, shard_t1 = 0;
+  uint64_t shard_e0 = 0, shard_e1 = 0;
+  int* own_order = nullptr;  // owned tiles, boundary tiles first
+  int own_count = 0;
+  float **push_x = nullptr, **push_m = nullptr, **push_v = nullptr, **push_vf = nullptr;  // [n-1] peers
+  double** push_sums = nullptr;                                                        // [n-1] peers
+  std::vector<void*> shard_ipc;
+  bool sharded_warmup() const;
+  void setup_shard();
+  void warmup_sharded(double lr, bool track, bool finalize, bool adam);
+  void sync_shards();  // collective: every owner's m and v slices into every rank
   bool strict = false;          // read-only finite pre-pass before any mutation (optimizers.cpp:99-117)
   bool m_valid = true;          // m buffer holds m (else: decompressed result * invc)
   bool mprev_separate = false;  // m_prev poked by the caller
