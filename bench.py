@@ -113,14 +113,17 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # algorithmic bytes per launch
 # ---------------------------------------------------------------------------
-def algorithmic_bytes(d: int, n: int, nw: int) -> dict:
+def algorithmic_bytes(d: int, n: int, nw: int, share: float = 1.0) -> dict:
+    """HBM bytes per step of each kernel (all its sub-launches); `share` is the
+    fraction of the tiles a rank updates in the warmup stage (1/n when the
+    multi-process warmup is owner-sharded)."""
     P = -(-d // n) * n
     c = P // n
     ns = nw
     return {
         # warmup stage: W1 g, m r/w, v r/w, x (24d); W2 m, v, x r/w (16d)
-        "w1_warmup_a": 24 * d,
-        "w2_warmup_b": 16 * d,
+        "w1_warmup_a": 24 * d * share,
+        "w2_warmup_b": 16 * d * share,
         # g (4d) + werr r/w (8P) + prev worker packet, prev result packet, new packet (3P/8)
         "k1_worker_compress": nw * (4 * d + 8 * P + 3 * P / 8),
         # serr r/w (8c) + n worker packets + prev server packet + new packet
@@ -345,10 +348,17 @@ def main():
     prof = cl.profile()
     cl.set_profiling(False)
     kern = {k: {"ms_per_launch": v[0] / max(v[1], 1), "launches": v[1]} for k, v in prof.items()}
-    ab = algorithmic_bytes(d, cl.n_workers(), nw)
+    # Owner-sharded warmup (multi-process over NVLink): a rank updates 1/n of the tiles.
+    sharded = (args.stage == "warmup" and world > 1 and cl.transport == "p2p"
+               and os.environ.get("BL_WARMUP_SHARD", "1") != "0")
+    ab = algorithmic_bytes(d, cl.n_workers(), nw, 1.0 / world if sharded else 1.0)
     peak, peak_kind = hbm_peak()
-    dom = max((k for k in kern if k in ab), key=lambda k: kern[k]["ms_per_launch"] * kern[k]["launches"])
-    achieved = ab[dom] / (kern[dom]["ms_per_launch"] * 1e-3) / 1e9
+
+    def step_ms(k):  # a kernel's time per step, summed over its sub-launches
+        return kern[k]["ms_per_launch"] * kern[k]["launches"] / args.steps
+
+    dom = max((k for k in kern if k in ab), key=step_ms)
+    achieved = ab[dom] / (step_ms(dom) * 1e-3) / 1e9
     traffic, traffic_src = None, None
     import glob
 
@@ -361,7 +371,7 @@ def main():
             traffic_src = os.path.relpath(caps[-1], ROOT)
     for k in kern:
         if k in ab:
-            kern[k]["gbs"] = ab[k] / (kern[k]["ms_per_launch"] * 1e-3) / 1e9
+            kern[k]["gbs"] = ab[k] / (step_ms(k) * 1e-3) / 1e9
     comm_ms = sum(kern.get(k, {}).get("ms_per_launch", 0) * kern.get(k, {}).get("launches", 0)
                   for k in ("k1_worker_compress", "finalize_scales", "nccl_alltoall", "k3_server_reduce",
                             "nccl_allgather")) / args.steps
@@ -416,6 +426,11 @@ def main():
                          "algorithmic_bytes": ab[dom]},
             "kernels": kern,
             "compressed_allreduce_ms": comm_ms,
+            # warmup stage over NVLink: the all-reduce moves 2 (n-1)/n * 4d bytes per
+            # direction per rank (reduce-scatter reads + allgather stores)
+            "warmup_nvlink_gbs_per_direction": (2 * (world - 1) / world * 4 * d / (ms * 1e-3) / 1e9)
+            if args.stage == "warmup" and world > 1 else None,
+            "warmup_sharded": sharded,
             "compressed_allreduce_algbw_gbs": 4 * d / (comm_ms * 1e-3) / 1e9 if comm_ms else None,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -262,7 +262,12 @@ bl_status bl_optimizer_step(bl_optimizer* o, bl_cluster* c, const float* const* 
 /* Device gradient buffer for worker i (zero-copy step with memory=BL_MEM_DEVICE). */
 float* bl_optimizer_grad_buffer(bl_optimizer* o, int32_t worker);
 
-/* layers()/mutable_layers() state access (optimizers.hpp:109-110), fused. */
+/* layers()/mutable_layers() state access (optimizers.hpp:109-110), fused.
+ * Multi-process clusters over NVLink keep m and v sharded by tile owner
+ * during the warmup stage (each rank updates 1/n of the tiles and stores
+ * the new x into every rank); reading BL_STATE_M or BL_STATE_V there first
+ * gathers every owner's slice, so every rank must make that call (the
+ * freeze step gathers m, v and v_frozen itself; x is always complete). */
 bl_status bl_optimizer_get_state(bl_optimizer* o, int32_t which, float* host_out);
 bl_status bl_optimizer_set_state(bl_optimizer* o, int32_t which, const float* host_in);
 /* c_avg, r_prev, MomentumScales::coeff per layer (any pointer may be NULL). */

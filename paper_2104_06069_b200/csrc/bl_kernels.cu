@@ -2171,10 +2171,16 @@ __device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint
 #define LOSSLESS_U 2  // 4-float groups per thread per iteration (n = 2, 4)
 #endif
 // Piece p's aligned body of the chunk body [a0, a1): [a0 + off(p), a0 + off(p+1)),
-// off(p) = (p * (a1 - a0) / pieces) rounded down to a multiple of 4 (off(pieces) = a1 - a0).
-__host__ __device__ __forceinline__ uint64_t piece_body_start(uint64_t a0, uint64_t a1, int pieces, int p) {
+// off(p) = F(p) * (a1 - a0) rounded down to a multiple of 4 (off(pieces) = a1 - a0),
+// F(p) = p / P (shape 0, equal pieces) or 1 - ((P - p) / P)^2 (shape 1,
+// linearly shrinking pieces: a short tail for the consumer of the last one).
+// Integer arithmetic: host and device agree exactly.
+__host__ __device__ __forceinline__ uint64_t piece_body_start(uint64_t a0, uint64_t a1, int pieces, int p,
+                                                              int shape = 0) {
   if (p >= pieces) return a1;
-  return a0 + ((static_cast<uint64_t>(p) * (a1 - a0) / static_cast<uint64_t>(pieces)) & ~3ull);
+  const uint64_t P = static_cast<uint64_t>(pieces), q = static_cast<uint64_t>(p);
+  const uint64_t num = shape == 1 ? P * P - (P - q) * (P - q) : q, den = shape == 1 ? P * P : P;
+  return a0 + ((num * (a1 - a0) / den) & ~3ull);
 }
 
 template <int NT>
@@ -2191,7 +2197,7 @@ __global__ void __launch_bounds__(256) k_lossless_p2p(const LosslessP2PParams p)
   constexpr int U = NT == 8 ? 1 : LOSSLESS_U;
   const int P = p.pieces > 0 ? p.pieces : 1;
   for (int pc = 0; pc < P; ++pc) {
-    const uint64_t b0 = piece_body_start(a0, a1, P, pc), b1 = piece_body_start(a0, a1, P, pc + 1);
+    const uint64_t b0 = piece_body_start(a0, a1, P, pc, p.shape), b1 = piece_body_start(a0, a1, P, pc + 1, p.shape);
     for (uint64_t k = b0 + 4 * tid; k < b1; k += 4 * nth * U) lossless_groups<NT, U>(p, k, 4 * nth, b1, inv_n);
     if (blockIdx.x == 0 && (pc == 0 || pc == P - 1)) {
       // unaligned head [lo, a0) (first piece) and tail [a1, hi) (last piece), one element per thread
@@ -3424,15 +3430,15 @@ int launch_small_collective(const SmallParams& p, int k1_mode, cudaStream_t s) {
   return al ? launch_small_t<2, true>(p, tiles, s) : launch_small_t<2, false>(p, tiles, s);
 }
 
-int lossless_piece(uint64_t lo, uint64_t hi, int pieces, uint64_t k) {
+int lossless_piece(uint64_t lo, uint64_t hi, int pieces, uint64_t k, int shape) {
   const uint64_t up = (lo + 3) & ~3ull, dn = hi & ~3ull;
   const uint64_t a0 = up < hi ? up : hi;
   const uint64_t a1 = dn > a0 ? dn : a0;
   if (k < a0) return 0;
   if (k >= a1) return pieces - 1;
   int p = static_cast<int>((k - a0) * static_cast<uint64_t>(pieces) / (a1 - a0));
-  while (p > 0 && k < piece_body_start(a0, a1, pieces, p)) --p;
-  while (p + 1 < pieces && k >= piece_body_start(a0, a1, pieces, p + 1)) ++p;
+  while (p > 0 && k < piece_body_start(a0, a1, pieces, p, shape)) --p;
+  while (p + 1 < pieces && k >= piece_body_start(a0, a1, pieces, p + 1, shape)) ++p;
   return p;
 }
 

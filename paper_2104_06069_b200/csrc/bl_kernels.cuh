@@ -251,6 +251,7 @@ struct LosslessP2PParams {
   // the average into the local output only (no allgather; hi == 0: chunk).
   uint64_t lo, hi;
   int local_only;
+  int shape;  // piece sizes: 0 equal, 1 linearly shrinking (piece_body_start)
 };
 
 struct W1Params {
@@ -367,7 +368,7 @@ int launch_verify(const float* raw, uint64_t c_pad, const uint32_t* pk, uint64_t
 int launch_lossless_p2p(const LosslessP2PParams& p, int sms, cudaStream_t s);
 // Piece boundaries of the piecewise lossless exchange: element k of chunk
 // [lo, hi) (global indices) belongs to piece lossless_piece(lo, hi, pieces, k).
-int lossless_piece(uint64_t lo, uint64_t hi, int pieces, uint64_t k);
+int lossless_piece(uint64_t lo, uint64_t hi, int pieces, uint64_t k, int shape = 0);
 // Block the stream until every rank's piece p is delivered (flags[base + q*pieces + p] >= epoch).
 int launch_wait_piece(const unsigned long long* flags, int base, int n, int pieces, int p,
                       unsigned long long epoch, unsigned long long* err, cudaStream_t s);

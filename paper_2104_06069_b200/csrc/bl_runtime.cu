@@ -1018,6 +1018,57 @@ void bl_optimizer::setup_shard() {
   own_order = reinterpret_cast<int*>(dalloc<float>(own.size()));
   if (!own.empty())
     cuda_check(cudaMemcpy(own_order, own.data(), own.size() * 4, cudaMemcpyHostToDevice), "own order");
+  const char* pe = std::getenv("BL_SHARD_PIECES");
+  // Defaults from the N=2 / N=4 sweeps (profiles/round2_shard_sweep_n*.txt).
+  shard_k = std::min(bl_cluster::kMaxPieces, std::max(1, pe ? std::atoi(pe) : (n == 2 ? 4 : 3)));
+  const int K = shard_k;
+  const char* se = std::getenv("BL_SHARD_SHAPE");
+  shard_shape = se ? std::atoi(se) : (n > 2 ? 1 : 0);
+  auto layer_of_tile = [&](int t) {
+    return static_cast<int>(std::upper_bound(lt_start_h.begin(), lt_start_h.end(), t) - lt_start_h.begin()) - 1;
+  };
+  // Reduce piece after which tile t's gradient is complete; a layer is local
+  // when all its tiles are owned here (its epilogue needs no peer partials).
+  std::vector<int> tpiece(static_cast<size_t>(tiles), 0), lpiece(static_cast<size_t>(L), 0);
+  for (int t : own) {
+    const int l = layer_of_tile(t);
+    const uint64_t e_last = std::min<uint64_t>(tile_elem(t) + kTile, off[l + 1]) - 1;
+    tpiece[t] = lossless_piece(shard_e0, shard_e1, K, e_last, shard_shape);
+    lpiece[l] = std::max(lpiece[l], tpiece[t]);
+  }
+  // Early W2 of local layers (measured slower: its NVLink stores compete
+  // with the reduce's reads; BL_SHARD_EARLY_W2=1 for experiments).
+  const bool early = std::getenv("BL_SHARD_EARLY_W2") != nullptr && std::atoi(std::getenv("BL_SHARD_EARLY_W2"));
+  auto local = [&](int l) { return early && lt_start_h[l] >= shard_t0 && lt_start_h[l + 1] <= shard_t1; };
+  // Buckets [0, K) by piece; bucket K = the rest (after the partials exchange).
+  auto bucketed = [&](const std::vector<int>& items, auto key, std::vector<int>* start) {
+    std::vector<std::vector<int>> b(static_cast<size_t>(K) + 1);
+    for (int it : items) b[static_cast<size_t>(key(it))].push_back(it);
+    std::vector<int> out;
+    start->assign(static_cast<size_t>(K) + 2, 0);
+    for (int q = 0; q <= K; ++q) {
+      (*start)[q] = static_cast<int>(out.size());
+      out.insert(out.end(), b[q].begin(), b[q].end());
+    }
+    (*start)[K + 1] = static_cast<int>(out.size());
+    return out;
+  };
+  std::vector<int> all_layers(static_cast<size_t>(L));
+  for (int l = 0; l < L; ++l) all_layers[l] = l;
+  const std::vector<int> w1o = bucketed(own, [&](int t) { return tpiece[t]; }, &own_w1_start);
+  const std::vector<int> w2o = bucketed(own, [&](int t) {
+    const int l = layer_of_tile(t);
+    return local(l) ? lpiece[l] : K;
+  }, &own_w2_start);
+  const std::vector<int> lwo = bucketed(all_layers, [&](int l) { return local(l) ? lpiece[l] : K; }, &own_lw_start);
+  auto upload = [](const std::vector<int>& h) {
+    int* dv = reinterpret_cast<int*>(dalloc<float>(h.size()));
+    if (!h.empty()) cuda_check(cudaMemcpy(dv, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "shard tables");
+    return dv;
+  };
+  own_w1_order = upload(w1o);
+  own_w2_order = upload(w2o);
+  own_lw_order = upload(lwo);
   std::vector<std::vector<void*>> peer;
   if (!cl->map_peer_buffers({x, m, v, vf, tile_sums}, &peer, &shard_ipc))
     fail(BL_ERR_UNSUPPORTED, "sharded warmup: a peer's optimizer state could not be mapped");
@@ -1072,48 +1123,40 @@ void bl_optimizer::warmup_sharded(double lr, bool track, bool finalize, bool ada
   lp.local_only = 1;
   const char* be = std::getenv("BL_LOSSLESS_BLOCK");
   lp.block = be ? std::atoi(be) : 0;
-  if (shard_e1 > shard_e0) {
-    cl->begin(KC_AVG, &a);
-    cl->end(KC_AVG, a, launch_lossless_p2p(lp, cl->sms, cl->stream));
+  // The reduce runs on the comm stream, raising a local flag per piece; W1
+  // follows on the main stream piece by piece (HBM work under the NVLink reads).
+  const int K = shard_k;
+  lp.pieces = K;
+  lp.shape = shard_shape;
+  lp.piece_flag_base = cl->piece_flag_base();
+  lp.piece_done = cl->piece_done;
+  const char* ce = std::getenv("BL_SHARD_CTAS_PER_SM");
+  lp.ctas = cl->sms * (ce ? std::max(1, std::atoi(ce)) : 2);
+  if (!cl->comm_stream) {
+    cuda_check(cudaStreamCreateWithFlags(&cl->comm_stream, cudaStreamNonBlocking), "comm stream");
+    cuda_check(cudaEventCreateWithFlags(&cl->ev_fork, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&cl->ev_join, cudaEventDisableTiming), "event");
   }
+  cuda_check(cudaEventRecord(cl->ev_fork, cl->stream), "fork");
+  cuda_check(cudaStreamWaitEvent(cl->comm_stream, cl->ev_fork, 0), "fork wait");
+  if (shard_e1 > shard_e0) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cl->profiling) {
+      e0 = cl->get_event();
+      cuda_check(cudaEventRecord(e0, cl->comm_stream), "cudaEventRecord");
+    }
+    cl->launches += static_cast<uint64_t>(launch_lossless_p2p(lp, cl->sms, cl->comm_stream));
+    cuda_check(cudaGetLastError(), "lossless (owned range)");
+    if (cl->profiling) {
+      e1 = cl->get_event();
+      cuda_check(cudaEventRecord(e1, cl->comm_stream), "cudaEventRecord");
+      cl->pending.push_back({KC_AVG, e0, e1});
+    }
+  }
+  cuda_check(cudaEventRecord(cl->ev_join, cl->comm_stream), "join");
   cl->ledger_lossless();
 
-  // W1 / epilogue / W2 parameters of the replicated path, restricted below.
-  W1Params w1{};
-  w1.gate = cl->err;
-  w1.lt = lt();
-  w1.lt.order = own_order;
-  w1.lt.count = own_count;
-  w1.gbar = cl->out;
-  w1.m = m;
-  w1.v = v;
-  w1.x = x;
-  w1.b1 = static_cast<float>(hp.beta1);
-  w1.omb1 = static_cast<float>(1.0 - hp.beta1);
-  w1.b2 = static_cast<float>(hp.beta2);
-  w1.omb2 = static_cast<float>(1.0 - hp.beta2);
-  w1.eta = static_cast<float>(hp.eta);
-  w1.wd = static_cast<float>(hp.weight_decay);
-  w1.tile_sums = tile_sums;
-  w1.adam = adam ? 1 : 0;
-  w1.worker_base = cl->rank;
-  if (own_count) {
-    cl->begin(KC_W1, &a);
-    cl->end(KC_W1, a, launch_w1(w1, cl->grid(own_count), cl->stream));
-  }
-  cl->begin(KC_AG, &a);
-  cl->end(KC_AG, a,
-          launch_push_range(tile_sums, push_sums, nn - 1, 4ull * static_cast<uint64_t>(shard_t0),
-                            4ull * static_cast<uint64_t>(shard_t1 - shard_t0), cl->err, cl->sms, cl->stream));
-  cl->begin(KC_AG, &a);
-  cl->end(KC_AG, a, launch_signal_peers(cl->d_peer_flags, sbase + cl->rank, nn, ep, cl->err, cl->stream));
-  cl->begin(KC_AG, &a);
-  cl->end(KC_AG, a, launch_wait_peers(cl->flags + sbase, nn, ep, cl->err, cl->stream));
-  warmup_kernels(lr, track, finalize, adam, -1, ep);  // the epilogue (all layers) and W2 (owned tiles)
-  cl->begin(KC_AG, &a);
-  cl->end(KC_AG, a, launch_signal_peers(cl->d_peer_flags, sbase + nn + cl->rank, nn, ep, cl->err, cl->stream));
-  cl->begin(KC_AG, &a);
-  cl->end(KC_AG, a, launch_wait_peers(cl->flags + sbase + nn, nn, ep, cl->err, cl->stream));
+  warmup_kernels(lr, track, finalize, adam, -1, ep);
   shard_stale = !finalize;
 }
 
@@ -1203,20 +1246,63 @@ void bl_optimizer::warmup_kernels(double lr, bool track, bool finalize, bool ada
   w2.eta = static_cast<float>(hp.eta);
   w2.wd = static_cast<float>(hp.weight_decay);
   w2.finalize = finalize ? 1 : 0;
-  if (K < 0) {  // owner-sharded: W1 ran on the owned tiles; epilogue, then W2 + allgather
-    cl->begin(KC_WEPI, &a);
-    cl->end(KC_WEPI, a, launch_wepilogue(we, cl->stream));
-    w2.lt.order = own_order;
-    w2.lt.count = own_count;
+  if (K < 0) {
+    // Owner-sharded (warmup_sharded): W1 on the owned tiles piece by piece
+    // behind the reduce; the local layers' epilogue and W2 (+ allgather) as
+    // soon as their last piece is in; then the tile partials to every rank,
+    // the remaining layers' epilogue and W2; then every owner delivered.
+    const int P = shard_k, nn = cl->n, sbase = cl->shard_flag_base();
+    w1.gbar = cl->out;
+    w1.err = nullptr;
     w2.push_x = push_x;
     w2.push_m = push_m;
     w2.push_v = push_v;
     w2.push_vf = push_vf;
-    w2.npush = cl->n - 1;
-    if (own_count) {
-      cl->begin(KC_W2, &a);
-      cl->end(KC_W2, a, launch_w2(w2, cl->grid(own_count), cl->stream));
+    w2.npush = nn - 1;
+    auto epi_w2 = [&](int q) {
+      if (const int cnt = own_lw_start[q + 1] - own_lw_start[q]) {
+        WEpiParams e = we;
+        e.layer_list = own_lw_order + own_lw_start[q];
+        e.count = cnt;
+        cl->begin(KC_WEPI, &a);
+        cl->end(KC_WEPI, a, launch_wepilogue(e, cl->stream));
+      }
+      if (const int cnt = own_w2_start[q + 1] - own_w2_start[q]) {
+        W2Params w = w2;
+        w.lt.order = own_w2_order + own_w2_start[q];
+        w.lt.count = cnt;
+        cl->begin(KC_W2, &a);
+        cl->end(KC_W2, a, launch_w2(w, cl->grid(cnt), cl->stream));
+      }
+    };
+    for (int p = 0; p < P; ++p) {
+      if (const int cnt = own_w1_start[p + 1] - own_w1_start[p]) {
+        cl->begin(KC_AG, &a);
+        cl->end(KC_AG, a,
+                launch_wait_piece(cl->flags, cl->piece_flag_base() + cl->rank * P, 1, P, p, ep, cl->err,
+                                  cl->stream));
+        W1Params q = w1;
+        q.lt.order = own_w1_order + own_w1_start[p];
+        q.lt.count = cnt;
+        cl->begin(KC_W1, &a);
+        cl->end(KC_W1, a, launch_w1(q, cl->grid(cnt), cl->stream));
+      }
+      epi_w2(p);
     }
+    cuda_check(cudaStreamWaitEvent(cl->stream, cl->ev_join, 0), "join");
+    cl->begin(KC_AG, &a);
+    cl->end(KC_AG, a,
+            launch_push_range(tile_sums, push_sums, nn - 1, 4ull * static_cast<uint64_t>(shard_t0),
+                              4ull * static_cast<uint64_t>(shard_t1 - shard_t0), cl->err, cl->sms, cl->stream));
+    cl->begin(KC_AG, &a);
+    cl->end(KC_AG, a, launch_signal_peers(cl->d_peer_flags, sbase + cl->rank, nn, ep, cl->err, cl->stream));
+    cl->begin(KC_AG, &a);
+    cl->end(KC_AG, a, launch_wait_peers(cl->flags + sbase, nn, ep, cl->err, cl->stream));
+    epi_w2(P);
+    cl->begin(KC_AG, &a);
+    cl->end(KC_AG, a, launch_signal_peers(cl->d_peer_flags, sbase + nn + cl->rank, nn, ep, cl->err, cl->stream));
+    cl->begin(KC_AG, &a);
+    cl->end(KC_AG, a, launch_wait_peers(cl->flags + sbase + nn, nn, ep, cl->err, cl->stream));
     return;
   }
   if (K == 0) {
@@ -2228,7 +2314,7 @@ void bl_optimizer_destroy(bl_optimizer* o) {
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (void* p : o->shard_ipc) cudaIpcCloseMemHandle(p);
-  void* shard_bufs[] = {o->own_order, o->push_x, o->push_m, o->push_v, o->push_vf, o->push_sums};
+  void* shard_bufs[] = {o->own_order, o->own_w1_order, o->own_w2_order, o->own_lw_order, o->push_x, o->push_m, o->push_v, o->push_vf, o->push_sums};
   for (void* p : shard_bufs)
     if (p) cudaFree(p);
   for (auto& gx : o->graph)

@@ -273,6 +273,16 @@ struct bl_optimizer {
   uint64_t shard_e0 = 0, shard_e1 = 0;
   int* own_order = nullptr;  // owned tiles, boundary tiles first
   int own_count = 0;
+  // W1 follows the owned-range reduce piece by piece: owned tiles bucketed by
+  // the reduce piece after which their gradient is complete.  Layers whose
+  // tiles are all owned here ("local") run their epilogue and W2 as soon as
+  // their last piece is in; the rest (bucket shard_k) after the exchange of
+  // tile partials.
+  int shard_k = 0, shard_shape = 0;
+  int* own_w1_order = nullptr;
+  int* own_w2_order = nullptr;
+  int* own_lw_order = nullptr;
+  std::vector<int> own_w1_start, own_w2_start, own_lw_start;  // [shard_k + 2]
   float **push_x = nullptr, **push_m = nullptr, **push_v = nullptr, **push_vf = nullptr;  // [n-1] peers
   double** push_sums = nullptr;                                                        // [n-1] peers
   std::vector<void*> shard_ipc;

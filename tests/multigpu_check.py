@@ -172,6 +172,12 @@ def optimizer_check(rank, world, local, new_uid, check, tp):
                 check(xs[r] == ref_x, f"{tp} optimizer x rank {r} t={t}")
                 check(trs[r] == st.c.tobytes() + st.r.tobytes() + st.v_norm.tobytes(),
                       f"optimizer trace rank {r} t={t}")
+        if t == 2:  # mid-warmup read of the owner-sharded m and v (collective)
+            for k in ("m", "v"):
+                vals = gather_bytes(opt.get(k).tobytes())
+                if rank == 0:
+                    ref = sopt.get(k).tobytes()
+                    check(all(v == ref for v in vals), f"{tp} optimizer mid-warmup {k}")
     for k in ("m", "v", "v_frozen"):
         vals = gather_bytes(opt.get(k).tobytes())
         if rank == 0:
