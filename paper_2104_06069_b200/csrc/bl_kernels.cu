@@ -2605,6 +2605,7 @@ __device__ __forceinline__ uint32_t ll_get(const uint2* p, uint32_t ep, unsigned
 // One K3 tile per CTA over LL-received worker words (k3_cta_tile's arithmetic
 // and order); server words go to the local plain result slot and, as LL
 // words, to every rank's result buffer.
+template <int NT>
 __device__ __forceinline__ void k3_cta_tile_ll(const SmallParams& sp, long long tile, uint32_t* sw, float* s_abs,
                                                float* s_cm, const float* scale, float es, double inv_n,
                                                bool& ok) {
@@ -2621,7 +2622,7 @@ __device__ __forceinline__ void k3_cta_tile_ll(const SmallParams& sp, long long 
   const uint2* inw = sp.ll_rx_mine + (i0 >> 5);
   constexpr int R = 4;
   const int r0 = R * wq;
-  constexpr int kMaxN = 8;
+  constexpr int kMaxN = NT;  // worker words held in registers (code size: the kernel runs once, i-cache cold)
   float4 raw[R];
   uint32_t sn[R], nb[R][kMaxN];
   uint2 lv[R][kMaxN];
@@ -2665,6 +2666,7 @@ __device__ __forceinline__ void k3_cta_tile_ll(const SmallParams& sp, long long 
 #pragma unroll
     for (int i = 0; i < kMaxN; ++i) nb[k][i] = lv[k][i].x;
   if (sp.ts && blockIdx.x == 0 && threadIdx.x == 0) sp.ts[10] = now_ns() + 0ull * nb[R - 1][0];
+  if (sp.ts && blockIdx.x == 0 && lane == 0) atomicMax(sp.ts + 13, now_ns() + 0ull * nb[R - 1][0]);  // last warp
   float cm = 0.0f;
 #pragma unroll
   for (int k = 0; k < R; ++k) {
@@ -2710,6 +2712,7 @@ __device__ __forceinline__ void k3_cta_tile_ll(const SmallParams& sp, long long 
   cm = warp_max(cm);
   if (lane == 0) s_cm[wq] = cm;
   __syncthreads();
+  if (sp.ts && blockIdx.x == 0 && threadIdx.x == 0) sp.ts[14] = now_ns();
   if (wq == 0) {
     double acc = 0.0;
     for (int r = 0; r < kRowsPerTile; ++r) {
@@ -2760,7 +2763,7 @@ __device__ __forceinline__ bool last_cta(unsigned int* c, bool* s_last) {
 // scale is formed by the CTA that finishes its phase last (last-CTA count).
 // Every per-element operation and reduction order is the unfused path's.
 // ---------------------------------------------------------------------------
-template <int MODE, bool ALIGNED>
+template <int MODE, bool ALIGNED, int NT>
 __global__ void __launch_bounds__(kBlock) k_small_collective(__grid_constant__ const SmallParams p) {
   __shared__ __align__(16) uint32_t s_words[128];  // the CTA's tile packet words
   __shared__ float s_scale[64];
@@ -2823,7 +2826,7 @@ __global__ void __launch_bounds__(kBlock) k_small_collective(__grid_constant__ c
     const float es = p.k3.es_dev ? __ldg(p.k3.es_dev) : p.k3.es_host;
     const double inv_n = 1.0 / static_cast<double>(n);
     for (long long tile = blockIdx.x; ok && tile < p.k3.tpc; tile += gridDim.x)
-      k3_cta_tile_ll(p, tile, s_words, s_abs, s_cm, s_scale, es, inv_n, ok);
+      k3_cta_tile_ll<NT>(p, tile, s_words, s_abs, s_cm, s_scale, es, inv_n, ok);
   }
   stamp(5);
   // 5. server scale: the last CTA combines the partials, sends it to every rank
@@ -3402,9 +3405,9 @@ int launch_build_stream(float* in, uint64_t stride, int nw, uint64_t d, const fl
   return 1;
 }
 
-template <int MODE, bool ALIGNED>
-static int launch_small_t(const SmallParams& p, long long tiles, cudaStream_t s) {
-  auto kern = k_small_collective<MODE, ALIGNED>;
+template <int MODE, bool ALIGNED, int NT>
+static int launch_small_nt(const SmallParams& p, long long tiles, cudaStream_t s) {
+  auto kern = k_small_collective<MODE, ALIGNED, NT>;
   static thread_local int cap = 0;  // co-resident blocks (cooperative launch)
   if (cap == 0) {
     int dev = 0, sms = 148, occ = 1;
@@ -3420,6 +3423,16 @@ static int launch_small_t(const SmallParams& p, long long tiles, cudaStream_t s)
   const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), grid, kBlock,
                                                     args, 0, s);
   return e == cudaSuccess ? 1 : -static_cast<int>(e);
+}
+
+template <int MODE, bool ALIGNED>
+static int launch_small_t(const SmallParams& p, long long tiles, cudaStream_t s) {
+  const int n = p.k1.n;
+#ifndef BL_SMALL_NT8  // (A/B knob: one instantiation for every n)
+  if (n <= 2) return launch_small_nt<MODE, ALIGNED, 2>(p, tiles, s);
+  if (n <= 4) return launch_small_nt<MODE, ALIGNED, 4>(p, tiles, s);
+#endif
+  return launch_small_nt<MODE, ALIGNED, 8>(p, tiles, s);
 }
 
 int launch_small_collective(const SmallParams& p, int k1_mode, cudaStream_t s) {

@@ -268,12 +268,12 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
                                     cudaGetErrorString(static_cast<cudaError_t>(-r)));
     end(KC_SMALL, a, r);
     if (ts_on) {
-      unsigned long long h[13];
+      unsigned long long h[15];
       cuda_check(cudaMemcpyAsync(h, small_ts, sizeof h, cudaMemcpyDeviceToHost, stream), "ts");
       cuda_check(cudaStreamSynchronize(stream), "ts");
       char line[256];
       int len = std::snprintf(line, sizeof line, "small_ts rank %d tiles %lld:", rank, static_cast<long long>(n) * tpc);
-      for (int k = 1; k < 13; ++k)
+      for (int k = 1; k < 15; ++k)
         len += std::snprintf(line + len, sizeof line - len, " %.2f", h[k] ? (h[k] - h[0]) * 1e-3 : -1.0);
       std::fprintf(stderr, "%s\n", line);  // one write per line (ranks share stderr)
     }
