@@ -2319,6 +2319,21 @@ __global__ void k_decompress(const uint32_t* res, int n, uint64_t c, uint64_t sl
   decompress_warps(res, n, c, slot, W, d, out, gw, nwarps, threadIdx.x & 31);
 }
 
+// last_cta over a counter that `target` arrivals complete (any CTAs).
+__device__ __forceinline__ bool last_of(unsigned int* c, unsigned int target, bool* s_last) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    *s_last = atomicAdd(c, 1u) == target - 1;
+    if (*s_last) {
+      *c = 0u;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return *s_last;
+}
+
 // ---------------------------------------------------------------------------
 // Fused small compressed collective (P2P transport): K1 -> worker scales ->
 // exchange -> K3 -> server scale -> exchange [-> decompress] in one
@@ -2782,26 +2797,36 @@ __global__ void __launch_bounds__(kBlock) k_small_collective(__grid_constant__ c
   stamp(0);
   const int n = p.k1.n;
   const uint32_t ep = p.ep32;
+  const long long total = static_cast<long long>(n) * p.k1.tpc;
+  const bool per_chunk = total <= static_cast<long long>(gridDim.x);
   bool ok = true;
   // 1. worker compression of every chunk of the local stream (plain words to
   //    the local slot, LL words into rank j's receive buffer)
   {
     const float es = p.k1.es_dev ? __ldg(p.k1.es_dev) : p.k1.es_host;
-    const long long total = static_cast<long long>(n) * p.k1.tpc;
     for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
       k1_cta_tile<MODE, ALIGNED>(p.k1, tile, s_words, s_abs, s_cm, es);
+      const int j = static_cast<int>(tile / p.k1.tpc);
       if (threadIdx.x < 32) {  // the tile's words, just written by this warp
-        const int j = static_cast<int>(tile / p.k1.tpc);
         const uint64_t w0 = static_cast<uint64_t>(tile - static_cast<long long>(j) * p.k1.tpc) * (kTile / 32);
         const uint4 v = reinterpret_cast<const uint4*>(p.k1.pk_cur + static_cast<size_t>(j) * p.k1.slot + w0)[lane];
         st_ll4(p.ll_rx[j] + p.ll_off + w0 + 4 * lane, v, ep);
       }
+      // 2. worker scale of chunk j (one tile per CTA): the CTA that finishes
+      //    the chunk's last tile combines its tile partials (k_finalize_scales'
+      //    order) and sends the scale to rank j -- the n scales form in parallel
+      if (per_chunk && last_of(p.cnt + 2 + j, static_cast<unsigned int>(p.k1.tpc), &s_last)) {
+        stamp(2);
+        if (threadIdx.x == 0) forward_grad_error(p.err, p.f1.peer_err, n);  // every rank raises
+        finalize_block256(p.f1, j, s_red);
+        if (threadIdx.x == 0)
+          st_ll1(p.ll_rx[j] + p.ll_off + p.k1.W, p.k1.pk_cur[static_cast<size_t>(j) * p.k1.slot + p.k1.W], ep);
+      }
     }
   }
   stamp(1);
-  // 2. worker scales: the last CTA combines every endpoint's tile partials
-  //    (k_finalize_scales' order) and sends scale e to rank e
-  if (last_cta(p.cnt, &s_last)) {
+  // 2'. several tiles per CTA: one count per CTA; the last CTA forms every scale
+  if (!per_chunk && last_cta(p.cnt, &s_last)) {
     stamp(2);
     if (threadIdx.x == 0) forward_grad_error(p.err, p.f1.peer_err, n);  // every rank raises
     for (int e = 0; e < n; ++e) {

@@ -221,7 +221,8 @@ struct SmallParams {
   const uint2* ll_rx_mine;  // this rank's LL rx, current parity, [n][slot]
   const uint2* ll_res_mine; // this rank's LL res, current parity, [n][slot]
   uint32_t* res_plain;      // this call's plain result packets [n][slot] (K5/K6, getters)
-  unsigned int* cnt;        // [2] CTA counters of the two last-CTA finalizes (self-resetting)
+  unsigned int* cnt;        // [2 + n] CTA counters of the last-CTA finalizes: [1] server scale,
+                            // [2 + j] chunk j's worker scale (self-resetting)
   unsigned int ep32;
 };
 

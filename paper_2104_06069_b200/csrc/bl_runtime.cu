@@ -504,7 +504,7 @@ void bl_cluster::setup_p2p(bool required) {
   flags = reinterpret_cast<unsigned long long*>(dalloc<double>(static_cast<size_t>(shard_flag_base()) + 2 * nn));
   piece_done = reinterpret_cast<unsigned int*>(dalloc<float>(kMaxPieces));
   lossless_done = reinterpret_cast<unsigned int*>(dalloc<float>(1));
-  small_bar = reinterpret_cast<unsigned int*>(dalloc<float>(2));
+  small_bar = reinterpret_cast<unsigned int*>(dalloc<float>(2 + nn));
   // LL buffers of the fused small collective, [2][n][slot] (word, epoch)
   // pairs; only sized when the small path can be taken.
   const size_t ll_words = static_cast<long long>(n) * tpc <= small_max_tiles() ? 2 * nn * slot : 1;
