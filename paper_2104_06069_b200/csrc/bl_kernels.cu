@@ -3445,6 +3445,8 @@ static int launch_small_nt(const SmallParams& p, long long tiles, cudaStream_t s
   if (want < p.k1.n) want = p.k1.n;  // one block per worker endpoint
   const int grid = static_cast<int>(std::min<long long>(want, cap));
   void* args[] = {const_cast<SmallParams*>(&p)};
+  // (A plain launch measured 0.5-1 us faster at 1-4 MB: not worth giving up
+  // the co-residency guarantee the LL polls rely on.)
   const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), grid, kBlock,
                                                     args, 0, s);
   return e == cudaSuccess ? 1 : -static_cast<int>(e);

@@ -4,7 +4,7 @@ N=${N:-2}
 out=gpurun_out/r2_${TAG:-nt}_ab_n$N.txt; : > $out
 for i in 1 2 3; do
   for v in new prev; do
-    if [ $v = prev ]; then export BL_LIB_PATH=$PWD/build/lib_prev.so; else unset BL_LIB_PATH; fi
+    if [ $v = prev ]; then export BL_LIB_PATH=$PWD/build/${ALT:-lib_prev.so}; else unset BL_LIB_PATH; fi
     timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr 127.0.0.1 --master-port 2961$i bench_sweep.py --sizes-mb ${SIZES:-1,2,4,8,16} --iters 50 > /tmp/s.txt 2>&1
     python - $v <<'PY' >> $out
 import json, sys
