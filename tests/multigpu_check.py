@@ -22,6 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2104_06069_b200 import bitlamb as bl  # noqa: E402
+from oracle import oracle as O  # noqa: E402  (the f32 C restatement: the parity checker)
 
 
 def gather_bytes(b: bytes) -> list[bytes]:
@@ -154,11 +155,17 @@ def optimizer_check(rank, world, local, new_uid, check, tp):
     if rank == 0:
         sim = bl.SimCluster(world, d, device=local)
         sopt = bl.Optimizer("onebit_lamb", sizes, hp, sim)
+        # and the f32 oracle directly (not only transitively through SIM mode)
+        ocl = O.Cluster("f32", world, d)
+        oopt = O.Optimizer("f32", "onebit_lamb", sizes,
+                           O.HyperParams(total_steps=steps, warmup_steps=warm, weight_decay=0.01,
+                                         scaled_error_feedback=True))
     rng = np.random.default_rng(7)
     x0 = (rng.standard_normal(d) * 0.02).astype(np.float32)
     opt.set("x", x0)
     if rank == 0:
         sopt.set("x", x0)
+        oopt.set("x", x0)
     sig = np.repeat(10.0 ** (-4 + 2 * rng.random(len(sizes))), sizes).astype(np.float32)
     for t in range(steps):
         g = (rng.standard_normal((world, d)) * sig).astype(np.float32)
@@ -168,6 +175,9 @@ def optimizer_check(rank, world, local, new_uid, check, tp):
         if rank == 0:
             st = sopt.step(g, t, 1e-3)
             ref_x = sopt.get("x").tobytes()
+            ost = oopt.step(g, t, 1e-3, ocl)
+            check(oopt.get("x").tobytes() == ref_x, f"{tp} oracle x t={t}")
+            check(np.array_equal(np.asarray(ost["c"]), np.asarray(st.c)), f"{tp} oracle trace c t={t}")
             for r in range(world):
                 check(xs[r] == ref_x, f"{tp} optimizer x rank {r} t={t}")
                 check(trs[r] == st.c.tobytes() + st.r.tobytes() + st.v_norm.tobytes(),
@@ -183,6 +193,7 @@ def optimizer_check(rank, world, local, new_uid, check, tp):
         if rank == 0:
             ref = sopt.get(k).tobytes()
             check(all(v == ref for v in vals), f"{tp} optimizer {k}")
+            check(oopt.get(k).tobytes() == ref, f"{tp} oracle {k}")
     opt.close()
     cl.close()
 
