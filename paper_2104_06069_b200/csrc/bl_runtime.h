@@ -110,7 +110,7 @@ struct bl_cluster {
   static long long small_max_tiles() {
     static const long long v = [] {
       const char* e = std::getenv("BL_SMALL_MAX_TILES");
-      return e ? std::atoll(e) : 1024ll;  // N=2/4 sweeps: the split kernels win from 32 MB per rank
+      return e ? std::atoll(e) : 2048ll;  // N=2/4 sweeps: the split kernels win from 64 MB per rank
     }();
     return v;
   }
