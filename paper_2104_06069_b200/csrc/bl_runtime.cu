@@ -368,6 +368,7 @@ bool bl_cluster::compressed(const K1Params* ovr, int k1_mode, float es_host, con
                  "ncclRecv");
     }
     nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    share_grad_error();  // K1's fused finite check, raised on every rank
     end(KC_A2A, a, 0);
     kin = rpk;
     in_s = 0;
@@ -535,6 +536,15 @@ void bl_cluster::setup_p2p(bool required) {
   transport = BL_TRANSPORT_P2P;
 }
 
+// NCCL transport: the lowest (worker << 40 | element) non-finite key over
+// ranks, so every rank reports the same gradient error (the P2P transport
+// forwards it with its flags).
+void bl_cluster::share_grad_error() {
+  if (mode != BL_MODE_NCCL || n == 1 || transport == BL_TRANSPORT_P2P) return;
+  nccl_check(ncclAllReduce(err + kErrGrad, err + kErrGrad, 1, ncclUint64, ncclMin, comm, stream),
+             "ncclAllReduce(gradient error)");
+}
+
 void bl_cluster::lossless(bool check_finite) {
   cudaEvent_t a;
   if (mode == BL_MODE_SIM || n == 1) {
@@ -590,9 +600,11 @@ void bl_cluster::lossless(bool check_finite) {
   nccl_check(ncclGroupEnd(), "ncclGroupEnd");
   end(KC_A2A, a, 0);
   if (check_finite) {
-    // check_gradients covers the rank's whole gradient, not just its chunk.
+    // check_gradients covers the rank's whole gradient, not just its chunk;
+    // the finding is raised on every rank (optimizers.cpp:99-117).
     begin(KC_AVG, &a);
     end(KC_AVG, a, launch_average(in, in_stride, 1, dim, nullptr, err, 1, rank, stream));
+    share_grad_error();
   }
   begin(KC_AVG, &a);
   end(KC_AVG, a, launch_average(lrecv, c_pad, n, c, out + static_cast<size_t>(rank) * c, err, 0,
@@ -1362,6 +1374,7 @@ void bl_optimizer::compressed_step(double lr, const float* stage_host) {
     cl->end(KC_AVG, a,
             launch_build_stream(cl->in, cl->in_stride, cl->nw, d, m_valid ? m : nullptr, off_dev, L,
                                 A, B, cl->err, cl->mode == BL_MODE_SIM ? 0 : cl->rank, cl->stream));
+    cl->share_grad_error();  // (the P2P exchange forwards it with its flags)
     cl->lossless(false);
     cl->ledger_compressed();
     cl->calls += 1;

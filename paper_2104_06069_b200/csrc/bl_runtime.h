@@ -200,6 +200,7 @@ struct bl_cluster {
                   const float* es_dev, float* dec_out = nullptr);
   void finish_compressed(float es_host, const float* es_dev);
   void lossless(bool check_finite);  // in -> out (averaged), ledger
+  void share_grad_error();           // NCCL transport: min-reduce the kErrGrad word over ranks
   // Warmup overlap (P2P, n > 1): the lossless exchange runs on comm_stream,
   // delivering the result in `pieces` pieces (flags at piece_flag_base); the
   // caller's consumers wait per piece on the main stream, then join.

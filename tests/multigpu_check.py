@@ -214,10 +214,31 @@ def optimizer_check(rank, world, local, new_uid, check, tp):
             raised = ""
         except Exception as exc:  # noqa: BLE001 - the message is checked below
             raised = str(exc)
-        if bad or (t == 2 and tp == "p2p"):
+        if t == 2:  # every rank, on both transports
             check("non-finite gradient" in raised and f"worker {world - 1}" in raised,
                   f"{tp} rank {rank}: non-finite gradient not reported: {raised!r}")
-        elif t < 2:
+        else:
+            check(raised == "", f"{tp} rank {rank} t={t} unexpected error {raised!r}")
+    opt.close()
+    cl.close()
+
+    # ... and in the compression stage (K1's fused check), after a one-step warmup.
+    cl = bl.SimCluster(world, d, mode="nccl", rank=rank, device=local, nccl_unique_id=new_uid(),
+                       transport=tp)
+    opt = bl.Optimizer("onebit_lamb", sizes, bl.HyperParams(total_steps=4, warmup_steps=1), cl)
+    for t in range(3):
+        g = (rng.standard_normal((1, d)) * sig).astype(np.float32)
+        if t == 2 and rank == world - 1:
+            g[0, d - 7] = np.inf
+        try:
+            opt.step(g, t, 1e-3)
+            raised = ""
+        except Exception as exc:  # noqa: BLE001 - the message is checked below
+            raised = str(exc)
+        if t == 2:
+            check("non-finite gradient" in raised and f"worker {world - 1}" in raised,
+                  f"{tp} rank {rank}: compression-stage non-finite gradient not reported: {raised!r}")
+        else:
             check(raised == "", f"{tp} rank {rank} t={t} unexpected error {raised!r}")
     opt.close()
     cl.close()
