@@ -1473,6 +1473,7 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
       continue;
     }
 
+    if (p.gen_list) continue;  // taken by k5_general
     double acc = 0.0;
     float mx = 0.0f;
     bool bad = false;
@@ -1686,6 +1687,7 @@ __global__ void __launch_bounds__(kBlock, K6_MINB) k6_update_b(const K6Params p)
       }
       continue;
     }
+    if (p.gen_list) continue;  // taken by k6_general
     for (int r = 0; r < kRowsPerTile; ++r) {
       const uint64_t ir = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r) * kRowElems;
       if (ir >= len) break;
@@ -1710,6 +1712,218 @@ __global__ void __launch_bounds__(kBlock, K6_MINB) k6_update_b(const K6Params p)
         set_comp(xn, q, __fadd_rn(comp(x, q), __fmul_rn(a, u)));          // :313 axpy
       }
       st_row4(p.x + kr, lane, s, xn, nv);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// General-path tiles of K5 / K6 for small problems (a tile across a chunk
+// boundary, or a layer off a 16-B boundary without the MISK kernels): one
+// warp per listed tile, on a side stream while the streaming kernel skips
+// them.  Such a tile is a chain of dependent rows; here every load of a
+// 4-row batch is issued first (branch-free: raw words and rows, decoded
+// after), so a batch costs one memory round trip instead of two per row.
+// Same per-element arithmetic and accumulation order as the streaming
+// kernels' general path (row_mg / ld_row4).
+// ---------------------------------------------------------------------------
+struct RowRaw {   // ld_row4's loads, not yet rotated
+  float4 lo, hi;
+};
+__device__ __forceinline__ RowRaw row_issue(const float* row, int lane, int s) {
+  const float* a = row - s;
+  RowRaw r;
+  r.lo = ld4(a + 4 * lane);
+  r.hi = (s != 0 && lane == 31) ? ld4(a + 128) : make_float4(0.f, 0.f, 0.f, 0.f);
+  return r;
+}
+__device__ __forceinline__ float4 row_finish(const RowRaw& r, int lane, int s) {  // = ld_row4
+  if (s == 0) return r.lo;
+  float hx = __shfl_down_sync(FULL, r.lo.x, 1);
+  float hy = __shfl_down_sync(FULL, r.lo.y, 1);
+  float hz = __shfl_down_sync(FULL, r.lo.z, 1);
+  if (lane == 31) {
+    hx = r.hi.x;
+    hy = r.hi.y;
+    hz = r.hi.z;
+  }
+  if (s == 1) return make_float4(r.lo.y, r.lo.z, r.lo.w, hx);
+  if (s == 2) return make_float4(r.lo.z, r.lo.w, hx, hy);
+  return make_float4(r.lo.w, hx, hy, hz);
+}
+struct BitsRaw {  // row_mg's loads, not yet decoded
+  uint32_t w0, w1, sw, sh;
+  uint64_t j;
+  bool cross;     // the row straddles a chunk end: decoded element by element
+};
+__device__ __forceinline__ BitsRaw bits_issue(const BitCursor& bc, uint64_t kr, int lane, uint64_t& j,
+                                              uint64_t& chunk_end) {
+  while (kr >= chunk_end) {
+    ++j;
+    chunk_end += bc.c;
+  }
+  BitsRaw b;
+  b.j = j;
+  b.cross = !(kr + (kRowElems - 1) < chunk_end || j + 1 >= static_cast<uint64_t>(bc.n));
+  const uint32_t* sl = bc.res + j * bc.slot;
+  const uint64_t i = kr - j * bc.c + 4 * lane;
+  b.sh = static_cast<uint32_t>(i & 31);
+  b.sw = __ldcg(sl + bc.W);
+  b.w0 = __ldcg(sl + (i >> 5));
+  b.w1 = __ldcg(sl + (i >> 5) + 1);
+  return b;
+}
+__device__ __forceinline__ float4 bits_finish(const BitCursor& bc, const BitsRaw& b, uint64_t kr, int lane,
+                                              float ic) {  // = row_mg
+  float4 out;
+  if (!b.cross) {
+    const float S = __uint_as_float(b.sw);
+    const float pos = S, neg = S == 0.0f ? 0.0f : -S;
+    const uint32_t nib = __funnelshift_r(b.w0, b.w1, b.sh) & 0xFu;
+    out.x = __fmul_rn(nib & 1u ? pos : neg, ic);
+    out.y = __fmul_rn(nib & 2u ? pos : neg, ic);
+    out.z = __fmul_rn(nib & 4u ? pos : neg, ic);
+    out.w = __fmul_rn(nib & 8u ? pos : neg, ic);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float S;
+      const uint32_t bit = bit_at(bc, kr + 4 * lane + q, &S);
+      set_comp(out, q, __fmul_rn(dec_value(bit, S), ic));
+    }
+  }
+  return out;
+}
+
+template <int MPREV>
+__global__ void __launch_bounds__(kBlock) k5_general(const K5Params p) {
+  if (gate_closed_call(p.err)) return;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const BitCursor cur{p.res_cur, p.c, p.slot, p.W, p.n};
+  const BitCursor prv{p.res_prev, p.c, p.slot, p.W, p.n};
+  for (long long i = gw; i < p.gen_count; i += nwarps) {
+    const long long tile = __ldg(p.gen_list + i);
+    const int l = __ldg(p.lt.tile_layer + tile);
+    const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
+    const uint64_t lo = __ldg(p.lt.off + l);
+    const uint64_t len = __ldg(p.lt.off + l + 1) - lo;
+    const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
+    const int s = static_cast<int>(lo & 3u);
+    const float ic = __ldg(p.invc + l);
+    uint64_t j = base / p.c, ce = (j + 1) * p.c;
+    uint64_t jp = j, cep = ce;
+    double acc = 0.0;
+    float mx = 0.0f;
+    bool bad = false;
+    constexpr int RB = 4;
+    for (int r0 = 0; r0 < kRowsPerTile; r0 += RB) {
+      const uint64_t ir0 = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r0) * kRowElems;
+      if (ir0 >= len) break;
+      const int nrow = static_cast<int>((len - ir0 + kRowElems - 1) / kRowElems);  // rows left in the layer
+      RowRaw rv[RB], rf[RB], rm[RB];
+      BitsRaw bc[RB], bp[RB];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {  // loads only
+        const uint64_t kr = base + static_cast<uint64_t>(r0 + k) * kRowElems;
+        if (k >= nrow) break;
+        rv[k] = row_issue(p.v + kr, lane, s);
+        rf[k] = row_issue(p.vf + kr, lane, s);
+        bc[k] = bits_issue(cur, kr, lane, j, ce);
+        if (MPREV == 0) rm[k] = row_issue(p.m + kr, lane, s);
+        else bp[k] = bits_issue(prv, kr, lane, jp, cep);
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        if (k >= nrow) break;
+        const uint64_t ir = ir0 + static_cast<uint64_t>(k) * kRowElems;
+        const uint64_t kr = base + static_cast<uint64_t>(r0 + k) * kRowElems;
+        const int nv = lane_valid(len, ir, lane);
+        const float4 v = row_finish(rv[k], lane, s);
+        const float4 vf = row_finish(rf[k], lane, s);
+        const float4 mg = bits_finish(cur, bc[k], kr, lane, ic);
+        const float4 mp = MPREV == 0 ? row_finish(rm[k], lane, s) : bits_finish(prv, bp[k], kr, lane, ic);
+        float4 vn;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          // :284-287 rec = inv*m_g + (-beta1*inv)*m_prev
+          const float rec = __fadd_rn(__fmul_rn(p.inv, comp(mg, q)), __fmul_rn(p.ninvb, comp(mp, q)));
+          // kernels.cpp:245 y = a*y + b*x*x
+          const float nvv = __fadd_rn(__fmul_rn(p.b2, comp(v, q)),
+                                      __fmul_rn(__fmul_rn(p.omb2, rec), rec));
+          set_comp(vn, q, nvv);
+          if (q < nv) {
+            bad |= !isfinite(rec);
+            const float den = nvv < p.floor_ ? p.floor_ : nvv;  // std::max(v, floor)
+            const float ratio = fabsf(comp(vf, q)) / den;
+            mx = mx < ratio ? ratio : mx;
+            acc += static_cast<double>(nvv) * static_cast<double>(nvv);
+          }
+        }
+        st_row4(p.v + kr, lane, s, vn, nv);
+      }
+    }
+    if (bad) flag(p.err, kErrRecon, static_cast<unsigned long long>(l));
+    acc = warp_bfly_sum(acc);
+    mx = warp_max(mx);
+    if (lane == 0) {
+      p.tile_v2[tile] = acc;
+      p.tile_max[tile] = mx;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k6_general(const K6Params p) {
+  if (gate_closed_call(p.gate)) return;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
+  const BitCursor cur{p.res_cur, p.c, p.slot, p.W, p.n};
+  for (long long i = gw; i < p.gen_count; i += nwarps) {
+    const long long tile = __ldg(p.gen_list + i);
+    const int l = __ldg(p.lt.tile_layer + tile);
+    const int t = static_cast<int>(tile - __ldg(p.lt.layer_tile_start + l));
+    const uint64_t lo = __ldg(p.lt.off + l);
+    const uint64_t len = __ldg(p.lt.off + l + 1) - lo;
+    const uint64_t base = lo + static_cast<uint64_t>(t) * kTile;
+    const int s = static_cast<int>(lo & 3u);
+    const float ic = __ldg(p.invc + l);
+    const float a = __ldg(p.coef_x + l);
+    uint64_t j = base / p.c, ce = (j + 1) * p.c;
+    constexpr int RB = 4;
+    for (int r0 = 0; r0 < kRowsPerTile; r0 += RB) {
+      const uint64_t ir0 = static_cast<uint64_t>(t) * kTile + static_cast<uint64_t>(r0) * kRowElems;
+      if (ir0 >= len) break;
+      const int nrow = static_cast<int>((len - ir0 + kRowElems - 1) / kRowElems);
+      RowRaw rx[RB], rf[RB];
+      BitsRaw bc[RB];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const uint64_t kr = base + static_cast<uint64_t>(r0 + k) * kRowElems;
+        if (k >= nrow) break;
+        rx[k] = row_issue(p.x + kr, lane, s);
+        rf[k] = row_issue(p.vf + kr, lane, s);
+        bc[k] = bits_issue(cur, kr, lane, j, ce);
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        if (k >= nrow) break;
+        const uint64_t ir = ir0 + static_cast<uint64_t>(k) * kRowElems;
+        const uint64_t kr = base + static_cast<uint64_t>(r0 + k) * kRowElems;
+        const int nv = lane_valid(len, ir, lane);
+        const float4 x = row_finish(rx[k], lane, s);
+        const float4 vf = row_finish(rf[k], lane, s);
+        const float4 mg = bits_finish(cur, bc[k], kr, lane, ic);
+        float4 xn;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          // kernels.cpp:229 precondition: m / (sqrt(v) + eta)
+          float u = __fdiv_rn(comp(mg, q), __fadd_rn(__fsqrt_rn(comp(vf, q)), p.eta));
+          if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x, q)));  // kernels.cpp:226 axpy
+          set_comp(xn, q, __fadd_rn(comp(x, q), __fmul_rn(a, u)));          // :313 axpy
+        }
+        st_row4(p.x + kr, lane, s, xn, nv);
+      }
     }
   }
 }
@@ -3353,6 +3567,14 @@ int launch_k5(const K5Params& p, int grid, cudaStream_t s) {
   return 1;
 }
 
+int launch_k5_general(const K5Params& p, cudaStream_t s) {
+  if (!p.gen_list || p.gen_count == 0) return 0;
+  const int g = (p.gen_count + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (p.res_prev) k5_general<1><<<g, kBlock, 0, s>>>(p);
+  else k5_general<0><<<g, kBlock, 0, s>>>(p);
+  return 1;
+}
+
 int launch_epilogue(const EpiParams& p, cudaStream_t s) {
   k_epilogue<<<p.L, 1024, 0, s>>>(p);
   return 1;
@@ -3361,6 +3583,12 @@ int launch_epilogue(const EpiParams& p, cudaStream_t s) {
 int launch_k6(const K6Params& p, int grid, cudaStream_t s) {
   if (p.lt.mis) k6_update_b<true><<<resident(k6_update_b<true>, grid), kBlock, 0, s>>>(p);
   else k6_update_b<false><<<resident(k6_update_b<false>, grid), kBlock, 0, s>>>(p);
+  return 1;
+}
+
+int launch_k6_general(const K6Params& p, cudaStream_t s) {
+  if (!p.gen_list || p.gen_count == 0) return 0;
+  k6_general<<<(p.gen_count + kWarpsPerBlock - 1) / kWarpsPerBlock, kBlock, 0, s>>>(p);
   return 1;
 }
 

@@ -163,6 +163,11 @@ struct K5Params {
   const float* dense;        // identity compressor: dense result (m_g = dense * invc)
   float* m_store;            // identity compressor: m <- m_g
   int norm_only;             // lamb_basic_1bit / onebit_adam: only ||v||^2 partials
+  // Tiles off the fast path (across a chunk boundary; misaligned without the
+  // MISK kernel), processed by k5_general on a side stream while the
+  // streaming kernel skips them; nullptr: the streaming kernel takes them.
+  const int* gen_list;
+  int gen_count;
 };
 
 struct EpiParams {
@@ -196,6 +201,8 @@ struct K6Params {
   float* x;
   float eta, wd;
   const float* dense;  // identity compressor: dense result
+  const int* gen_list; // as K5Params (k6_general)
+  int gen_count;
 };
 
 // Fused small compressed collective (P2P transport, one cooperative kernel).
@@ -334,8 +341,11 @@ int launch_k1_phase(const K1Params& p, int mode, int phase, cudaStream_t s);
 int launch_finalize(const FinalizeParams& p, int count, cudaStream_t s);
 int launch_k3(const K3Params& p, int grid, cudaStream_t s);
 int launch_k5(const K5Params& p, int grid, cudaStream_t s);
+// The listed general-path tiles (K5Params::gen_list), concurrent with launch_k5 on another stream.
+int launch_k5_general(const K5Params& p, cudaStream_t s);
 int launch_epilogue(const EpiParams& p, cudaStream_t s);
 int launch_k6(const K6Params& p, int grid, cudaStream_t s);
+int launch_k6_general(const K6Params& p, cudaStream_t s);
 int launch_w1(const W1Params& p, int grid, cudaStream_t s);
 int launch_wepilogue(const WEpiParams& p, cudaStream_t s);
 int launch_w2(const W2Params& p, int grid, cudaStream_t s);

@@ -615,14 +615,29 @@ void bl_cluster::lossless(bool check_finite) {
   end(KC_AG, a, 0);
 }
 
+void bl_cluster::ensure_side_stream() {
+  if (comm_stream) return;
+  cuda_check(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking), "comm stream");
+  cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+}
+
+// Run `launch` on the side stream after everything enqueued so far on the
+// main stream; join_side() makes the main stream wait for it.
+void bl_cluster::fork_side(const std::function<int(cudaStream_t)>& launch) {
+  ensure_side_stream();
+  cuda_check(cudaEventRecord(ev_fork, stream), "fork");
+  cuda_check(cudaStreamWaitEvent(comm_stream, ev_fork, 0), "fork wait");
+  launches += static_cast<uint64_t>(launch(comm_stream));
+  cuda_check(cudaGetLastError(), "side-stream launch");
+  cuda_check(cudaEventRecord(ev_join, comm_stream), "join");
+}
+void bl_cluster::join_side() { cuda_check(cudaStreamWaitEvent(stream, ev_join, 0), "join wait"); }
+
 unsigned long long bl_cluster::lossless_pieces(bool check_finite, int pieces) {
   const unsigned long long ep = ++lcalls;
   const int nn = n;
-  if (!comm_stream) {
-    cuda_check(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking), "comm stream");
-    cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
-    cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
-  }
+  ensure_side_stream();
   cudaEvent_t a;
   begin(KC_A2A, &a);
   end(KC_A2A, a, launch_signal_peers(d_peer_flags, 2 * nn + rank, nn, ep, err, stream));
@@ -1144,11 +1159,7 @@ void bl_optimizer::warmup_sharded(double lr, bool track, bool finalize, bool ada
   lp.piece_done = cl->piece_done;
   const char* ce = std::getenv("BL_SHARD_CTAS_PER_SM");
   lp.ctas = cl->sms * (ce ? std::max(1, std::atoi(ce)) : 2);
-  if (!cl->comm_stream) {
-    cuda_check(cudaStreamCreateWithFlags(&cl->comm_stream, cudaStreamNonBlocking), "comm stream");
-    cuda_check(cudaEventCreateWithFlags(&cl->ev_fork, cudaEventDisableTiming), "event");
-    cuda_check(cudaEventCreateWithFlags(&cl->ev_join, cudaEventDisableTiming), "event");
-  }
+  cl->ensure_side_stream();
   cuda_check(cudaEventRecord(cl->ev_fork, cl->stream), "fork");
   cuda_check(cudaStreamWaitEvent(cl->comm_stream, cl->ev_fork, 0), "fork wait");
   if (shard_e1 > shard_e0) {
@@ -1362,6 +1373,35 @@ void bl_optimizer::warmup_kernels(double lr, bool track, bool finalize, bool ada
   }
 }
 
+// The streaming K5/K6 kernels' fast-path test per tile (bl_kernels.cu),
+// evaluated on the host: a tile inside one result chunk, on a 16-B
+// boundary unless the MISK kernels run.  The rest go to k5/k6_general when
+// the problem is small enough for their chains to set the kernels' time
+// (BL_GENERAL_SPLIT_MAX_TILES, default 16384 tiles; larger problems hide
+// them behind the boundary-first streaming kernels).
+void bl_optimizer::ensure_gen_tiles() {
+  if (gen_c == cl->c) return;
+  gen_c = cl->c;
+  gen_n = 0;
+  const char* e = std::getenv("BL_GENERAL_SPLIT_MAX_TILES");
+  if (tiles > (e ? std::atoll(e) : 16384ll)) return;
+  std::vector<int> gen;
+  for (int l = 0; l < L; ++l) {
+    const uint64_t lo = off[l], len = off[l + 1] - lo;
+    const bool aligned = mis_layers || (lo & 3u) == 0;
+    for (uint64_t k = 0; k < len; k += kTile) {
+      const uint64_t base = lo + k, tvalid = std::min<uint64_t>(len - k, kTile);
+      const uint64_t ce = (base / cl->c + 1) * cl->c;
+      if (!(aligned && base + tvalid <= ce)) gen.push_back(lt_start_h[l] + static_cast<int>(k / kTile));
+    }
+  }
+  if (gen.empty()) return;
+  if (gen_tiles) cudaFree(gen_tiles);
+  gen_tiles = reinterpret_cast<int*>(dalloc<float>(gen.size()));
+  cuda_check(cudaMemcpy(gen_tiles, gen.data(), gen.size() * 4, cudaMemcpyHostToDevice), "general tiles");
+  gen_n = static_cast<int>(gen.size());
+}
+
 void bl_optimizer::compressed_step(double lr, const float* stage_host) {
   const bool identity = cl->cfg.compressor != BL_COMPRESSOR_ONEBIT;
   // optimizers.cpp:271-303: ratio rule (onebit_lamb), c = c_avg (basic), c = 1 (adam)
@@ -1430,8 +1470,15 @@ void bl_optimizer::compressed_step(double lr, const float* stage_host) {
   k5.tile_max = tile_max;
   k5.tile_v2 = tile_sums;
   k5.err = cl->err;
+  if (!identity) ensure_gen_tiles();
+  if (!identity && emode == 0 && gen_n) {
+    k5.gen_list = gen_tiles;
+    k5.gen_count = gen_n;
+  }
   cl->begin(KC_K5, &a);
+  if (k5.gen_list) cl->fork_side([&](cudaStream_t s2) { return launch_k5_general(k5, s2); });
   cl->end(KC_K5, a, launch_k5(k5, cl->grid(tiles), cl->stream));
+  if (k5.gen_list) cl->join_side();
 
   EpiParams ep{};
   ep.gate = cl->err;
@@ -1472,8 +1519,14 @@ void bl_optimizer::compressed_step(double lr, const float* stage_host) {
   k6.eta = static_cast<float>(hp.eta);
   k6.wd = static_cast<float>(hp.weight_decay);
   k6.dense = identity ? cl->out : nullptr;
+  if (!identity && gen_n) {
+    k6.gen_list = gen_tiles;
+    k6.gen_count = gen_n;
+  }
   cl->begin(KC_K6, &a);
+  if (k6.gen_list) cl->fork_side([&](cudaStream_t s2) { return launch_k6_general(k6, s2); });
   cl->end(KC_K6, a, launch_k6(k6, cl->grid(tiles), cl->stream));
+  if (k6.gen_list) cl->join_side();
 
   m_valid = identity;  // identity: m stored by K5; one-bit: m == decompressed result * invc
   mprev_separate = false;
@@ -2327,6 +2380,7 @@ void bl_optimizer_destroy(bl_optimizer* o) {
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (void* p : o->shard_ipc) cudaIpcCloseMemHandle(p);
+  if (o->gen_tiles) cudaFree(o->gen_tiles);
   void* shard_bufs[] = {o->own_order, o->own_w1_order, o->own_w2_order, o->own_lw_order, o->push_x, o->push_m, o->push_v, o->push_vf, o->push_sums};
   for (void* p : shard_bufs)
     if (p) cudaFree(p);

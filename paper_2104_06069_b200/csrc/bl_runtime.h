@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/bitlamb_b200.h"
@@ -218,6 +219,9 @@ struct bl_cluster {
   unsigned int* piece_done = nullptr;  // [kMaxPieces]
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  void ensure_side_stream();
+  void fork_side(const std::function<int(cudaStream_t)>& launch);
+  void join_side();
   void refresh_stats();
   void check_errors(const bl_optimizer* opt);
   void sync_and_check(const bl_optimizer* opt);
@@ -291,6 +295,13 @@ struct bl_optimizer {
   void setup_shard();
   void warmup_sharded(double lr, bool track, bool finalize, bool adam);
   void sync_shards();  // collective: every owner's m and v slices into every rank
+  // K5/K6 tiles off the fast path for the cluster's chunk length (built on
+  // first use; small problems only): taken by k5_general / k6_general on
+  // the side stream instead of the streaming kernels.
+  int* gen_tiles = nullptr;
+  int gen_n = 0;
+  uint64_t gen_c = 0;
+  void ensure_gen_tiles();
   bool strict = false;          // read-only finite pre-pass before any mutation (optimizers.cpp:99-117)
   bool m_valid = true;          // m buffer holds m (else: decompressed result * invc)
   bool mprev_separate = false;  // m_prev poked by the caller
