@@ -3503,8 +3503,12 @@ bool k1_uses_bulk(const K1Params& p, int mode) {
   // pipeline; 8-byte-aligned chunks load as float2 on the register path,
   // which measures faster there (BERT-L sim2: 1.35 vs 1.42 ms).
   // A single chunk (n == 1) starts at element 0 and is always aligned.
+  // Small problems (at most 16384 K1 tiles, e.g. config 0: 7.8K) are
+  // latency-bound and measure faster on the register path (config 0 K1
+  // 123 -> 105 us, profiles/round2_cfg0_k1.txt).
   const bool misaligned = (p.c & 1u) != 0 && p.n > 1;
-  return mode != 1 && (mode == 0 || p.tile_layer) && (misaligned || bulk_all()) && !bulk_none();
+  const bool large = static_cast<long long>(p.nw) * p.n * p.tpc > 16384ll;
+  return mode != 1 && (mode == 0 || p.tile_layer) && ((misaligned && large) || bulk_all()) && !bulk_none();
 }
 
 int launch_k1_phase(const K1Params& p, int mode, int phase, cudaStream_t s) {
