@@ -521,8 +521,9 @@ __device__ __forceinline__ void k1_tile(const K1Params& p, long long tile, int l
           if (MODE == 0) {
             v = comp(g[k], q);
           } else {
-            const float mq = __fmul_rn((rn[k] >> q) & 1u ? pos_m : neg_m, IC);   // fusion.cpp:143
-            v = __fadd_rn(__fmul_rn(A, mq), __fmul_rn(B, comp(g[k], q)));     // kernels.cpp:253
+            // A * (m_q = +-S2 * invc): two values per tile, hoisted (same products)
+            const float ap = __fmul_rn(A, __fmul_rn(pos_m, IC)), an = __fmul_rn(A, __fmul_rn(neg_m, IC));
+            v = __fadd_rn((rn[k] >> q) & 1u ? ap : an, __fmul_rn(B, comp(g[k], q)));  // fusion.cpp:143, kernels.cpp:253
           }
           const float rec = (wn[k] >> q) & 1u ? Sp : -Sp;
           const float delta = __fsub_rn(comp(raw[k], q), rec);                // compression.cpp:194
@@ -938,8 +939,8 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
         if (MODE == 0) {
           v = comp(g, q);
         } else {
-          const float mq = __fmul_rn((rn >> q) & 1u ? pos_m : neg_m, IC);  // fusion.cpp:143
-          v = __fadd_rn(__fmul_rn(A, mq), __fmul_rn(B, comp(g, q)));     // kernels.cpp:253
+          const float ap = __fmul_rn(A, __fmul_rn(pos_m, IC)), an = __fmul_rn(A, __fmul_rn(neg_m, IC));
+          v = __fadd_rn((rn >> q) & 1u ? ap : an, __fmul_rn(B, comp(g, q)));  // fusion.cpp:143, kernels.cpp:253
         }
         const float rec = (wn >> q) & 1u ? Sp : -Sp;
         const float delta = __fsub_rn(comp(raw, q), rec);    // compression.cpp:194
@@ -1425,9 +1426,11 @@ __global__ void __launch_bounds__(kBlock, K5_MINB) k5_update_a(const K5Params p)
             float4 vn;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const float mg = __fmul_rn((nc[k] >> q) & 1u ? pos : neg, ic);
-              const float mp = MPREV ? __fmul_rn((np[k] >> q) & 1u ? posp : negp, ic) : comp(mpb[k], q);
-              const float rec = __fadd_rn(__fmul_rn(p.inv, mg), __fmul_rn(p.ninvb, mp));
+              // inv * m_g and ninvb * m_prev take two values each per tile: hoisted (same products)
+              const float gp = __fmul_rn(p.inv, __fmul_rn(pos, ic)), gn = __fmul_rn(p.inv, __fmul_rn(neg, ic));
+              const float pp = __fmul_rn(p.ninvb, __fmul_rn(posp, ic)), pn = __fmul_rn(p.ninvb, __fmul_rn(negp, ic));
+              const float rec = __fadd_rn((nc[k] >> q) & 1u ? gp : gn,
+                                          MPREV ? ((np[k] >> q) & 1u ? pp : pn) : __fmul_rn(p.ninvb, comp(mpb[k], q)));
               const float nvv = __fadd_rn(__fmul_rn(p.b2, comp(v[k], q)),
                                           __fmul_rn(__fmul_rn(p.omb2, rec), rec));
               set_comp(vn, q, nvv);
@@ -1655,7 +1658,8 @@ __global__ void __launch_bounds__(kBlock, K6_MINB) k6_update_b(const K6Params p)
             float4 xn;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const float mg = __fmul_rn((nc[k] >> q) & 1u ? pos : neg, ic);
+              const float mgp = __fmul_rn(pos, ic), mgn = __fmul_rn(neg, ic);  // hoisted (same products)
+              const float mg = (nc[k] >> q) & 1u ? mgp : mgn;
               float u = __fdiv_rn(mg, __fadd_rn(__fsqrt_rn(comp(vf[k], q)), p.eta));
               if (p.wd > 0.0f) u = __fadd_rn(u, __fmul_rn(p.wd, comp(x[k], q)));
               set_comp(xn, q, __fadd_rn(comp(x[k], q), __fmul_rn(a, u)));
@@ -2661,8 +2665,8 @@ __device__ __forceinline__ void k1_cta_tile(const K1Params& p, long long tile, u
       if (MODE == 0) {
         v = comp(g[k], q);
       } else {
-        const float mq = __fmul_rn((rn[k] >> q) & 1u ? pos_m : neg_m, IC);  // fusion.cpp:143
-        v = __fadd_rn(__fmul_rn(A, mq), __fmul_rn(B, comp(g[k], q)));    // kernels.cpp:253
+        const float ap = __fmul_rn(A, __fmul_rn(pos_m, IC)), an = __fmul_rn(A, __fmul_rn(neg_m, IC));
+        v = __fadd_rn((rn[k] >> q) & 1u ? ap : an, __fmul_rn(B, comp(g[k], q)));  // fusion.cpp:143, kernels.cpp:253
       }
       const float rec = (wn[k] >> q) & 1u ? Sp : -Sp;
       const float delta = __fsub_rn(comp(raw[k], q), rec);               // compression.cpp:194
