@@ -1065,7 +1065,7 @@ __device__ __forceinline__ void flush_server_words(const K3Params& p, uint32_t* 
 }
 
 #ifndef K3_R1
-#define K3_R1 8
+#define K3_R1 16  // n = 1: 16-row batches at 2 CTAs/SM (A/B: profiles/round2_k3n1_ab.txt)
 #endif
 #ifndef K3_R2
 #define K3_R2 4
@@ -1083,7 +1083,10 @@ __device__ __forceinline__ void flush_server_words(const K3Params& p, uint32_t* 
 #define K3_B2 3
 #endif
 #define K3_ROWS(NT) ((NT) == 1 ? K3_R1 : (NT) == 2 ? K3_R2 : (NT) == 4 ? K3_R4 : 4)
-#define K3_MINB(NT) ((NT) == 1 ? (K3_R1 == 8 ? 3 : 4) : (NT) == 2 ? K3_B2 : (NT) == 4 ? K3_B4 : (NT) == 8 ? K3_B8 : 2)
+#ifndef K3_B1
+#define K3_B1 (K3_R1 == 16 ? 2 : K3_R1 == 8 ? 3 : 4)
+#endif
+#define K3_MINB(NT) ((NT) == 1 ? K3_B1 : (NT) == 2 ? K3_B2 : (NT) == 4 ? K3_B4 : (NT) == 8 ? K3_B8 : 2)
 template <int NT>
 __global__ void __launch_bounds__(kBlock, K3_MINB(NT)) k3_server_reduce(const K3Params p) {
   if (gate_closed_call(p.err)) return;
