@@ -1589,18 +1589,22 @@ __global__ void __launch_bounds__(1024) k_epilogue(const EpiParams p) {
     last = atomicAdd(p.counter, 1u) == static_cast<unsigned>(L - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double c_sum = 0.0;  // ascending over layers; L2 loads, 8 in flight
-    int k = 0;
-    for (; k + 8 <= p.L; k += 8) {
-      double v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = __ldcg(p.trace + k + q);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) c_sum += v[q];
-    }
-    for (; k < p.L; ++k) c_sum += __ldcg(p.trace + k);
+  if (!last) return;
+  // c_mean over layers, added in ascending layer order by one thread; the
+  // whole block stages 1024 layers' c at a time in shared memory (one L2
+  // round trip per 1024 layers instead of one per 8).
+  __shared__ double s_c[1024];
+  __threadfence();
+  double c_sum = 0.0;
+  for (int k0 = 0; k0 < p.L; k0 += 1024) {
+    const int cnt = p.L - k0 < 1024 ? p.L - k0 : 1024;
+    if (static_cast<int>(threadIdx.x) < cnt) s_c[threadIdx.x] = __ldcg(p.trace + k0 + threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int q = 0; q < cnt; ++q) c_sum += s_c[q];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     p.cmean[1] = p.cmean[0];
     const double cm = c_sum / static_cast<double>(p.L);
     p.cmean[0] = cm < p.floor_ ? p.floor_ : cm;
