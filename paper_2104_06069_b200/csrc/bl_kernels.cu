@@ -980,16 +980,20 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 4) k1_bulk(const K1Params p) 
 // s = a[t0] + a[t0 + step] + ... (t < t1), added in that order from 0; the
 // loads are issued 8 at a time so the dependent fp64 adds do not wait on
 // one load each (the canonical stripe sums of finalize / epilogues).
+#ifndef STRIPE_BATCH
+#define STRIPE_BATCH 8  // (16 measured slower in the scale finalize: profiles/round2_fin16_ab.txt)
+#endif
 template <int STEP = 1024>
 __device__ __forceinline__ double stripe_sum(const double* a, long long t0, long long t1) {
+  constexpr int B = STRIPE_BATCH;  // loads in flight per thread
   double s = 0.0;
   long long t = t0;
-  for (; t + 7ll * STEP < t1; t += 8ll * STEP) {
-    double v[8];
+  for (; t + (B - 1ll) * STEP < t1; t += static_cast<long long>(B) * STEP) {
+    double v[B];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = a[t + k * STEP];
+    for (int k = 0; k < B; ++k) v[k] = a[t + k * STEP];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += v[k];
+    for (int k = 0; k < B; ++k) s += v[k];
   }
   for (; t < t1; t += STEP) s += a[t];
   return s;
