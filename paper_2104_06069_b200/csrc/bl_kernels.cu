@@ -1099,6 +1099,7 @@ __global__ void __launch_bounds__(kBlock, K3_MINB(NT)) k3_server_reduce(const K3
   __shared__ __align__(16) uint32_t s_words[kWarpsPerBlock][128];
   // 2^n-entry server-average table for n in {4, 8} (per warp, per chunk)
   constexpr bool kTable = NT >= 4;
+  constexpr bool kSel = NT == 1 || NT == 2;  // averages by select from per-tile values
   __shared__ float s_tab[kWarpsPerBlock][kTable ? (1 << (NT > 0 ? NT : 1)) : 1];
   int tab_chunk = -1;
   uint32_t* sw = s_words[threadIdx.x >> 5];
@@ -1168,10 +1169,36 @@ __global__ void __launch_bounds__(kBlock, K3_MINB(NT)) k3_server_reduce(const K3
         __syncwarp();
         tab_chunk = j;
       }
+      // n <= 2: the 2^n possible averages of this tile's chunk, formed once
+      // per tile by the same ascending fp64 sum and *1/n (compression.cpp:83-89)
+      float tv[4] = {0.f, 0.f, 0.f, 0.f};
+      if (kSel) {
+#pragma unroll
+        for (int e = 0; e < (1 << (NT > 0 ? NT : 1)); ++e) {
+          double a = 0.0;
+#pragma unroll
+          for (int i = 0; i < (NT > 0 ? NT : 1); ++i) {
+            const float S = s_scale[wib][i];
+            if (S != 0.0f) a += ((e >> i) & 1) ? static_cast<double>(S) : -static_cast<double>(S);
+          }
+          tv[e] = static_cast<float>(a * inv_n);
+        }
+      }
 #pragma unroll
         for (int k = 0; k < R; ++k) {
           float4 avg;
-          if (kTable) {
+          if (kSel) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t b0 = (wn[k][0] >> q) & 1u;
+              if (NT == 1) {
+                set_comp(avg, q, b0 ? tv[1] : tv[0]);
+              } else {
+                const uint32_t b1 = (wn[k][NT > 1 ? 1 : 0] >> q) & 1u;
+                set_comp(avg, q, b1 ? (b0 ? tv[3] : tv[2]) : (b0 ? tv[1] : tv[0]));
+              }
+            }
+          } else if (kTable) {
             uint32_t x = 0;  // nibble of worker i at bits 4i..4i+3
 #pragma unroll
             for (int i = 0; i < NT; ++i) x |= (wn[k][i] & 0xFu) << (4 * i);
