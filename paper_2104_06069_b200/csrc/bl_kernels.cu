@@ -2939,28 +2939,53 @@ __device__ __forceinline__ void k3_cta_tile_ll(const SmallParams& sp, long long 
   if (sp.ts && blockIdx.x == 0 && threadIdx.x == 0) sp.ts[10] = now_ns() + 0ull * nb[R - 1][0];
   if (sp.ts && blockIdx.x == 0 && lane == 0) atomicMax(sp.ts + 13, now_ns() + 0ull * nb[R - 1][0]);  // last warp
   float cm = 0.0f;
+  // n == 2: the 4 possible averages, formed once (same fp64 sum and *1/n)
+  constexpr bool kSel = NT == 2;
+  float tv[4] = {0.f, 0.f, 0.f, 0.f};
+  if (kSel && n == 2) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      double a = 0.0;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float S = scale[i];
+        if (S != 0.0f) a += ((e >> i) & 1) ? static_cast<double>(S) : -static_cast<double>(S);
+      }
+      tv[e] = static_cast<float>(a * inv_n);
+    }
+  }
 #pragma unroll
   for (int k = 0; k < R; ++k) {
     const int r = r0 + k;
     const uint64_t ir = i0 + static_cast<uint64_t>(r) * kRowElems;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    auto add = [&](int i, uint32_t word) {  // compression.cpp:83-89, ascending workers
-      const float S = scale[i];
-      const uint32_t b = (word >> (4 * (lane & 7))) & 0xFu;
-      if (S != 0.0f) {
-        const double Sd = S;
-        a0 += (b & 1u) ? Sd : -Sd;
-        a1 += (b & 2u) ? Sd : -Sd;
-        a2 += (b & 4u) ? Sd : -Sd;
-        a3 += (b & 8u) ? Sd : -Sd;
-      }
-    };
+    float4 avg;
+    if (kSel && n == 2) {
+      const uint32_t sh = 4 * (lane & 7);
 #pragma unroll
-    for (int i = 0; i < kMaxN; ++i)
-      if (i < n) add(i, nb[k][i]);
-    for (int i = kMaxN; i < n; ++i) add(i, ll_get(inw + i * p.slot + 4 * r + (lane >> 3), sp.ep32, sp.err, ok));
-    const float4 avg = make_float4(static_cast<float>(a0 * inv_n), static_cast<float>(a1 * inv_n),
-                                   static_cast<float>(a2 * inv_n), static_cast<float>(a3 * inv_n));
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t b0 = (nb[k][0] >> (sh + q)) & 1u, b1 = (nb[k][kSel ? 1 : 0] >> (sh + q)) & 1u;
+        set_comp(avg, q, b1 ? (b0 ? tv[3] : tv[2]) : (b0 ? tv[1] : tv[0]));
+      }
+    } else {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      auto add = [&](int i, uint32_t word) {  // compression.cpp:83-89, ascending workers
+        const float S = scale[i];
+        const uint32_t b = (word >> (4 * (lane & 7))) & 0xFu;
+        if (S != 0.0f) {
+          const double Sd = S;
+          a0 += (b & 1u) ? Sd : -Sd;
+          a1 += (b & 2u) ? Sd : -Sd;
+          a2 += (b & 4u) ? Sd : -Sd;
+          a3 += (b & 8u) ? Sd : -Sd;
+        }
+      };
+#pragma unroll
+      for (int i = 0; i < kMaxN; ++i)
+        if (i < n) add(i, nb[k][i]);
+      for (int i = kMaxN; i < n; ++i) add(i, ll_get(inw + i * p.slot + 4 * r + (lane >> 3), sp.ep32, sp.err, ok));
+      avg = make_float4(static_cast<float>(a0 * inv_n), static_cast<float>(a1 * inv_n),
+                        static_cast<float>(a2 * inv_n), static_cast<float>(a3 * inv_n));
+    }
     uint32_t nib = 0;
     float4 rawn, ab;
 #pragma unroll
