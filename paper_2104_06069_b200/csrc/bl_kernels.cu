@@ -1202,13 +1202,24 @@ __global__ void __launch_bounds__(kBlock, K3_MINB(NT)) k3_server_reduce(const K3
             uint32_t x = 0;  // nibble of worker i at bits 4i..4i+3
 #pragma unroll
             for (int i = 0; i < NT; ++i) x |= (wn[k][i] & 0xFu) << (4 * i);
+            if (NT == 4) {
+              // 4x4 bit transpose (worker-major -> element-major): element q's
+              // 4-bit worker pattern lands at bits 4q..4q+3
+              uint32_t t = (x ^ (x >> 3)) & 0x0A0Au;
+              x = x ^ t ^ (t << 3);
+              t = (x ^ (x >> 6)) & 0x00CCu;
+              x = x ^ t ^ (t << 6);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {  // gather bits q, q+4, ... -> n-bit pattern
-              uint32_t y = (x >> q) & 0x11111111u;
-              y = (y | (y >> 3)) & 0x03030303u;
-              y = (y | (y >> 6)) & 0x000F000Fu;
-              y = (y | (y >> 12)) & 0xFFu;
-              set_comp(avg, q, s_tab[wib][y]);
+              for (int q = 0; q < 4; ++q) set_comp(avg, q, s_tab[wib][(x >> (4 * q)) & 0xFu]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {  // gather bits q, q+4, ... -> n-bit pattern
+                uint32_t y = (x >> q) & 0x11111111u;
+                y = (y | (y >> 3)) & 0x03030303u;
+                y = (y | (y >> 6)) & 0x000F000Fu;
+                y = (y | (y >> 12)) & 0xFFu;
+                set_comp(avg, q, s_tab[wib][y]);
+              }
             }
           } else {
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
