@@ -363,6 +363,9 @@ def main():
     import glob
 
     caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    final = os.path.join(ROOT, "profiles", "round2_final_traffic.json")  # the end-of-round capture
+    if os.path.exists(final):
+        caps.append(final)
     if caps and args.workload == "bert-large" and cl.n_workers() == 1:
         with open(caps[-1]) as f:
             tj = json.load(f)
