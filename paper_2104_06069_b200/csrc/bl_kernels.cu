@@ -2383,6 +2383,16 @@ __global__ void k_average(const float* in, uint64_t stride, int n, uint64_t len,
 // non-finite element of rank q is reported into rank q's own error word.
 // U groups of 4 elements (k0, k0 + step, ...) per thread: all peers' loads
 // of all groups are issued before any is consumed (NVLink latency).
+#ifndef LOSSLESS_U
+#define LOSSLESS_U 2  // 4-float groups per thread per iteration (n = 2, 4)
+#endif
+// Peer gradient loads of the lossless exchange (A/B knob: -DLOSSLESS_LD256
+// asks the L2 for 256-byte sectors, i.e. fewer, larger NVLink reads).
+#ifdef LOSSLESS_LD256
+#define LOSSLESS_LD(ptr) ldg_ro(ptr)
+#else
+#define LOSSLESS_LD(ptr) __ldcg(reinterpret_cast<const float4*>(ptr))
+#endif
 template <int NT, int U>
 __device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint64_t k0,
                                                 uint64_t step, uint64_t end, double inv_n) {
@@ -2401,7 +2411,7 @@ __device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint
       const uint64_t k = k0 + u * step;
 #pragma unroll
       for (int q = 0; q < kN; ++q)
-        if (q < m && k < end) g[u][q] = __ldcg(reinterpret_cast<const float4*>(p.peer_in[q0 + q] + k));
+        if (q < m && k < end) g[u][q] = LOSSLESS_LD(p.peer_in[q0 + q] + k);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -2434,9 +2444,7 @@ __device__ __forceinline__ void lossless_groups(const LosslessP2PParams& p, uint
   }
 }
 
-#ifndef LOSSLESS_U
-#define LOSSLESS_U 2  // 4-float groups per thread per iteration (n = 2, 4)
-#endif
+
 // Piece p's aligned body of the chunk body [a0, a1): [a0 + off(p), a0 + off(p+1)),
 // off(p) = F(p) * (a1 - a0) rounded down to a multiple of 4 (off(pieces) = a1 - a0),
 // F(p) = p / P (shape 0, equal pieces) or 1 - ((P - p) / P)^2 (shape 1,
