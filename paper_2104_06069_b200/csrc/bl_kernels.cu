@@ -2533,6 +2533,122 @@ __global__ void k_push_range(const T* src, T* const* dst, int ndst, uint64_t off
   __threadfence_system();
 }
 
+// Push-based owner-sharded exchange (ShardPushParams).  Owner r's range
+// [E_r, E_r+1) splits like the lossless kernel's chunk: a 16-B aligned body in
+// `pieces` pieces (piece_body_start) plus the unaligned head (piece 0) and
+// tail (last piece).  Slot offsets are relative to E_r rounded down to 4, so
+// body stores are 16-B aligned.
+__device__ __forceinline__ void shard_piece(uint64_t E0, uint64_t E1, int P, int pc, int shape, uint64_t* b0,
+                                            uint64_t* b1, uint64_t* h0, uint64_t* h1, uint64_t* t0,
+                                            uint64_t* t1) {
+  const uint64_t up = (E0 + 3) & ~3ull, dn = E1 & ~3ull;
+  const uint64_t a0 = up < E1 ? up : E1;
+  const uint64_t a1 = dn > a0 ? dn : a0;
+  *b0 = piece_body_start(a0, a1, P, pc, shape);
+  *b1 = piece_body_start(a0, a1, P, pc + 1, shape);
+  *h0 = E0;
+  *h1 = pc == 0 ? a0 : E0;
+  *t0 = a1;
+  *t1 = pc == P - 1 ? E1 : a1;
+}
+
+__global__ void __launch_bounds__(256) k_shard_push(const ShardPushParams p) {
+  if (gate_closed_call(p.gate)) return;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (int pc = 0; pc < p.pieces; ++pc) {
+    for (int r = 0; r < p.n; ++r) {
+      if (r == p.rank) continue;
+      const uint64_t E0 = p.e_all[r], E1 = p.e_all[r + 1];
+      uint64_t b0, b1, h0, h1, t0, t1;
+      shard_piece(E0, E1, p.pieces, pc, p.shape, &b0, &b1, &h0, &h1, &t0, &t1);
+      float* dst = p.peer_stg[r] + static_cast<uint64_t>(p.rank) * p.S - (E0 & ~3ull);  // dst[e], e in [E0, E1)
+      // 4 groups of 4 floats per thread: all loads in flight before the stores
+      for (uint64_t k = b0 + 4 * tid; k < b1; k += 16 * nth) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t ku = k + 4 * u * nth;
+          if (ku < b1) v[u] = __ldcs(reinterpret_cast<const float4*>(p.in + ku));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t ku = k + 4 * u * nth;
+          if (ku < b1) *reinterpret_cast<float4*>(dst + ku) = v[u];
+        }
+      }
+      for (uint64_t k = h0 + tid; k < h1; k += nth) dst[k] = p.in[k];
+      for (uint64_t k = t0 + tid; k < t1; k += nth) dst[k] = p.in[k];
+    }
+    // Piece delivered to every owner: CTA barrier, one system fence per CTA,
+    // the CTA count; the last CTA raises "piece pc from this rank" everywhere
+    // (at itself too: the owner waits for all n).
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      if (atomicAdd(p.piece_done + pc, 1u) == gridDim.x - 1) {
+        p.piece_done[pc] = 0u;
+        __threadfence_system();
+        for (int q = 0; q < p.n; ++q)
+          st_relaxed_sys(p.peer_flags[q] + p.piece_flag_base + p.rank * p.pieces + pc, p.epoch);
+      }
+    }
+  }
+}
+
+// Owner side: piece `piece` of [E0, E1), the ascending-rank fp64 average of
+// the own gradient and the staged slots (k_lossless_p2p's arithmetic, and its
+// check_gradients finding per sending rank).
+__global__ void __launch_bounds__(256) k_shard_reduce(const ShardReduceParams p) {
+  if (gate_closed_call(p.err)) return;
+  const double inv_n = 1.0 / static_cast<double>(p.n);
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t nth = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint64_t b0, b1, h0, h1, t0, t1;
+  shard_piece(p.E0, p.E1, p.pieces, p.piece, p.shape, &b0, &b1, &h0, &h1, &t0, &t1);
+  const uint64_t base = p.E0 & ~3ull;
+  auto src = [&](int q, uint64_t k) -> const float* {
+    return q == p.rank ? p.in + k : p.stg + static_cast<uint64_t>(q) * p.S + (k - base);
+  };
+  for (uint64_t k = b0 + 4 * tid; k < b1; k += 4 * nth) {
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = 0; q < p.n; ++q) {
+      const float4 g = __ldcs(reinterpret_cast<const float4*>(src(q, k)));
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x = comp(g, e);
+        if (!isfinite(x) && k + e < p.d) flag(p.err, kErrGrad, (static_cast<unsigned long long>(q) << 40) | (k + e));
+        a[e] += static_cast<double>(x);
+      }
+    }
+    *reinterpret_cast<float4*>(p.out + k) =
+        make_float4(static_cast<float>(a[0] * inv_n), static_cast<float>(a[1] * inv_n),
+                    static_cast<float>(a[2] * inv_n), static_cast<float>(a[3] * inv_n));
+  }
+  auto scalar = [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t k = lo + tid; k < hi; k += nth) {
+      double acc = 0.0;
+      for (int q = 0; q < p.n; ++q) {
+        const float x = *src(q, k);
+        if (!isfinite(x) && k < p.d) flag(p.err, kErrGrad, (static_cast<unsigned long long>(q) << 40) | k);
+        acc += static_cast<double>(x);
+      }
+      p.out[k] = static_cast<float>(acc * inv_n);
+    }
+  };
+  scalar(h0, h1);
+  scalar(t0, t1);
+  if (p.piece == p.pieces - 1) {  // every rank raises a non-finite gradient (optimizers.cpp:99-117)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(p.done, 1u) == gridDim.x - 1) {
+      *p.done = 0u;
+      __threadfence();
+      forward_grad_error(p.err, p.peer_err, p.n);
+    }
+  }
+}
+
 // Consumer side of the piecewise exchange: every rank's piece p delivered.
 __global__ void k_wait_piece(const unsigned long long* flags, int base, int n, int pieces, int pc,
                              unsigned long long epoch, unsigned long long* err) {
@@ -3834,6 +3950,15 @@ int launch_push_range(const double* src, double* const* dst, int ndst, uint64_t 
   const uint64_t want = (count + 255) / 256;
   k_push_range<double><<<static_cast<int>(want < static_cast<uint64_t>(4 * sms) ? want : 4 * sms), 256, 0, s>>>(
       src, dst, ndst, off, count, gate);
+  return 1;
+}
+
+int launch_shard_push(const ShardPushParams& p, int ctas, cudaStream_t s) {
+  k_shard_push<<<ctas, 256, 0, s>>>(p);
+  return 1;
+}
+int launch_shard_reduce(const ShardReduceParams& p, int sms, cudaStream_t s) {
+  k_shard_reduce<<<2 * sms, 256, 0, s>>>(p);
   return 1;
 }
 

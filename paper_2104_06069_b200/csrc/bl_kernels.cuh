@@ -262,6 +262,36 @@ struct LosslessP2PParams {
   int shape;  // piece sizes: 0 equal, 1 linearly shrinking (piece_body_start)
 };
 
+// Push-based owner-sharded warmup exchange (BL_SHARD_PUSH=1): every rank
+// stores each owner's range of its gradient into that owner's staging slot
+// [rank] (NVLink stores), per piece, and raises "piece p from rank q" at the
+// owner; the owner reduces its range from its own gradient and the staged
+// slots (k_shard_reduce).  Piece boundaries are the lossless kernel's.
+struct ShardPushParams {
+  const float* in;                         // local gradient
+  float* const* peer_stg;                  // [n] every rank's staging buffer [n][S]
+  const uint64_t* e_all;                   // [n + 1] owned element ranges
+  uint64_t S;                              // staging floats per sender slot
+  int n, rank, pieces, shape;
+  unsigned long long* const* peer_flags;   // [n]
+  int piece_flag_base;
+  unsigned long long epoch;
+  unsigned int* piece_done;                // [pieces] local CTA counters (self-resetting)
+  const unsigned long long* gate;
+};
+struct ShardReduceParams {
+  const float* in;                         // local gradient
+  const float* stg;                        // local staging buffer [n][S]
+  uint64_t S, E0, E1, d;
+  int n, rank, pieces, shape, piece;
+  float* out;
+  unsigned long long* err;
+  unsigned long long* const* peer_err;     // [n]: the last piece forwards a non-finite finding
+  unsigned int* done;                      // local CTA counter (self-resetting)
+};
+int launch_shard_push(const ShardPushParams& p, int ctas, cudaStream_t s);
+int launch_shard_reduce(const ShardReduceParams& p, int sms, cudaStream_t s);
+
 struct W1Params {
   const unsigned long long* gate;
   LayerTiles lt;

@@ -1096,9 +1096,29 @@ void bl_optimizer::setup_shard() {
   own_w1_order = upload(w1o);
   own_w2_order = upload(w2o);
   own_lw_order = upload(lwo);
+  const char* pu = std::getenv("BL_SHARD_PUSH");
+  shard_push = pu && std::atoi(pu) != 0;  // (must agree on every rank)
+  std::vector<void*> to_map = {x, m, v, vf, tile_sums};
+  if (shard_push) {
+    std::vector<uint64_t> e_all(static_cast<size_t>(n) + 1);
+    for (int q = 0; q <= n; ++q) e_all[q] = tile_elem(static_cast<int>(static_cast<long long>(tiles) * q / n));
+    stg_S = 0;
+    for (int q = 0; q < n; ++q) stg_S = std::max<uint64_t>(stg_S, e_all[q + 1] - (e_all[q] & ~3ull));
+    stg_S = (stg_S + 7) & ~3ull;
+    stg = dalloc<float>(static_cast<size_t>(n) * stg_S);
+    e_all_dev = reinterpret_cast<uint64_t*>(dalloc<double>(e_all.size()));
+    cuda_check(cudaMemcpy(e_all_dev, e_all.data(), e_all.size() * 8, cudaMemcpyHostToDevice), "ranges");
+    to_map.push_back(stg);
+  }
   std::vector<std::vector<void*>> peer;
-  if (!cl->map_peer_buffers({x, m, v, vf, tile_sums}, &peer, &shard_ipc))
+  if (!cl->map_peer_buffers(to_map, &peer, &shard_ipc))
     fail(BL_ERR_UNSUPPORTED, "sharded warmup: a peer's optimizer state could not be mapped");
+  if (shard_push) {
+    d_peer_stg = reinterpret_cast<float**>(dalloc<double>(static_cast<size_t>(n)));
+    cuda_check(cudaMemcpy(d_peer_stg, peer[5].data(), static_cast<size_t>(n) * sizeof(void*),
+                          cudaMemcpyHostToDevice),
+               "staging table");
+  }
   auto table = [&](int k) {
     std::vector<void*> others;
     for (int q = 0; q < n; ++q)
@@ -1162,13 +1182,33 @@ void bl_optimizer::warmup_sharded(double lr, bool track, bool finalize, bool ada
   cl->ensure_side_stream();
   cuda_check(cudaEventRecord(cl->ev_fork, cl->stream), "fork");
   cuda_check(cudaStreamWaitEvent(cl->comm_stream, cl->ev_fork, 0), "fork wait");
-  if (shard_e1 > shard_e0) {
+  if (shard_push || shard_e1 > shard_e0) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (cl->profiling) {
       e0 = cl->get_event();
       cuda_check(cudaEventRecord(e0, cl->comm_stream), "cudaEventRecord");
     }
-    cl->launches += static_cast<uint64_t>(launch_lossless_p2p(lp, cl->sms, cl->comm_stream));
+    if (shard_push) {
+      ShardPushParams sp{};
+      sp.in = cl->in;
+      sp.peer_stg = d_peer_stg;
+      sp.e_all = e_all_dev;
+      sp.S = stg_S;
+      sp.n = nn;
+      sp.rank = cl->rank;
+      sp.pieces = K;
+      sp.shape = shard_shape;
+      sp.peer_flags = cl->d_peer_flags;
+      sp.piece_flag_base = cl->piece_flag_base();
+      sp.epoch = ep;
+      sp.piece_done = cl->piece_done;
+      sp.gate = cl->err;
+      const char* pc = std::getenv("BL_SHARD_PUSH_CTAS_PER_SM");
+      cl->launches += static_cast<uint64_t>(
+          launch_shard_push(sp, cl->sms * (pc ? std::max(1, std::atoi(pc)) : 4), cl->comm_stream));
+    } else {
+      cl->launches += static_cast<uint64_t>(launch_lossless_p2p(lp, cl->sms, cl->comm_stream));
+    }
     cuda_check(cudaGetLastError(), "lossless (owned range)");
     if (cl->profiling) {
       e1 = cl->get_event();
@@ -1299,11 +1339,35 @@ void bl_optimizer::warmup_kernels(double lr, bool track, bool finalize, bool ada
       }
     };
     for (int p = 0; p < P; ++p) {
-      if (const int cnt = own_w1_start[p + 1] - own_w1_start[p]) {
+      if (shard_push) {  // every rank's piece p staged here, then the local reduce of piece p
         cl->begin(KC_AG, &a);
-        cl->end(KC_AG, a,
-                launch_wait_piece(cl->flags, cl->piece_flag_base() + cl->rank * P, 1, P, p, ep, cl->err,
-                                  cl->stream));
+        cl->end(KC_AG, a, launch_wait_piece(cl->flags, cl->piece_flag_base(), nn, P, p, ep, cl->err, cl->stream));
+        ShardReduceParams rp{};
+        rp.in = cl->in;
+        rp.stg = stg;
+        rp.S = stg_S;
+        rp.E0 = shard_e0;
+        rp.E1 = shard_e1;
+        rp.d = d;
+        rp.n = nn;
+        rp.rank = cl->rank;
+        rp.pieces = P;
+        rp.shape = shard_shape;
+        rp.piece = p;
+        rp.out = cl->out;
+        rp.err = cl->err;
+        rp.peer_err = cl->d_peer_err;
+        rp.done = cl->lossless_done;
+        cl->begin(KC_AVG, &a);
+        cl->end(KC_AVG, a, launch_shard_reduce(rp, cl->sms, cl->stream));
+      }
+      if (const int cnt = own_w1_start[p + 1] - own_w1_start[p]) {
+        if (!shard_push) {
+          cl->begin(KC_AG, &a);
+          cl->end(KC_AG, a,
+                  launch_wait_piece(cl->flags, cl->piece_flag_base() + cl->rank * P, 1, P, p, ep, cl->err,
+                                    cl->stream));
+        }
         W1Params q = w1;
         q.lt.order = own_w1_order + own_w1_start[p];
         q.lt.count = cnt;
@@ -2381,6 +2445,9 @@ void bl_optimizer_destroy(bl_optimizer* o) {
     if (p) cudaFree(p);
   for (void* p : o->shard_ipc) cudaIpcCloseMemHandle(p);
   if (o->gen_tiles) cudaFree(o->gen_tiles);
+  void* push_bufs[] = {o->stg, o->e_all_dev, o->d_peer_stg};
+  for (void* p : push_bufs)
+    if (p) cudaFree(p);
   void* shard_bufs[] = {o->own_order, o->own_w1_order, o->own_w2_order, o->own_lw_order, o->push_x, o->push_m, o->push_v, o->push_vf, o->push_sums};
   for (void* p : shard_bufs)
     if (p) cudaFree(p);

@@ -290,6 +290,13 @@ struct bl_optimizer {
   std::vector<int> own_w1_start, own_w2_start, own_lw_start;  // [shard_k + 2]
   float **push_x = nullptr, **push_m = nullptr, **push_v = nullptr, **push_vf = nullptr;  // [n-1] peers
   double** push_sums = nullptr;                                                        // [n-1] peers
+  // BL_SHARD_PUSH=1: the exchange is a push into each owner's staging slots
+  // (k_shard_push) + a local reduce per piece (k_shard_reduce) instead of pulls.
+  bool shard_push = false;
+  float* stg = nullptr;          // [n][stg_S] staged ranges of every rank's gradient
+  uint64_t stg_S = 0;
+  uint64_t* e_all_dev = nullptr; // [n + 1] every rank's owned range
+  float** d_peer_stg = nullptr;  // [n]
   std::vector<void*> shard_ipc;
   bool sharded_warmup() const;
   void setup_shard();
