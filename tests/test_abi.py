@@ -142,6 +142,10 @@ def test_bench_byte_model():
     assert 44.5 < total / 336_226_108 < 45.5  # ~44.9 B/param at n=1
     ab8 = bench.algorithmic_bytes(336_226_108, 8, 1)
     assert ab8["k3_server_reduce"] < ab["k3_server_reduce"] / 7
+    # owner-sharded warmup: a rank updates 1/n of the tiles
+    ab4 = bench.algorithmic_bytes(336_226_108, 4, 1, share=0.25)
+    assert ab4["w1_warmup_a"] == ab["w1_warmup_a"] / 4 and ab4["w2_warmup_b"] == ab["w2_warmup_b"] / 4
+    assert ab4["k5_update_a"] == ab["k5_update_a"]  # the compression stage stays replicated
 
 
 def test_bench_reference_arm_prints_contract_line():
